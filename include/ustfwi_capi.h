@@ -1,0 +1,192 @@
+/*
+ * ustfwi_capi.h — C ABI of the B200-native TD-FWI gradient engine (libustfwi_b200.so).
+ *
+ * This is the drop-in boundary for the hot path of arXiv 2102.00755 as implemented by
+ * the reference C++ library (/root/reference/proj/include/ustfwi). Every entry point
+ * names the reference interface it replaces (file:line, paths relative to
+ * proj/include/ustfwi/). Plain pointers and sizes only: no torch, no C++ types.
+ * The C++ drop-in headers (include/ustfwi/*.hpp) wrap these calls back into the
+ * reference's value types and exceptions; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *   - Every function returns a status: USTFWI_OK (0) or one of USTFWI_ERR_*.
+ *     USTFWI_ERR_INVALID   <-> std::invalid_argument   (grid.hpp:35-51, medium.hpp:41-57)
+ *     USTFWI_ERR_NUMERICAL <-> ustfwi::NumericalError  (core/errors.hpp:10-12)
+ *     The message of the last failure is returned by ustfwi_last_error() (per thread).
+ *   - Host buffers are owned by the caller. The API is fp64 at the boundary
+ *     (field.hpp:38,89); device arithmetic is fp32 (loss and adjoint-source scan fp64).
+ *   - Fields are row-major with the last axis fastest (field.hpp:14-17). 1-D and 2-D
+ *     grids are accepted and run as 3-D grids with leading singleton axes.
+ *   - A context is the device analogue of one SpectralEngine + its WaveSteppers
+ *     (engine.hpp:14-16, "one engine per worker"): not thread-safe, one CUDA stream.
+ *   - There is NO CPU fallback: without a usable sm_100 device, ustfwi_gpu_create fails
+ *     with USTFWI_ERR_CUDA.
+ */
+#ifndef USTFWI_CAPI_H
+#define USTFWI_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define USTFWI_API __attribute__((visibility("default")))
+#else
+#define USTFWI_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define USTFWI_OK 0
+#define USTFWI_ERR_INVALID 1
+#define USTFWI_ERR_NUMERICAL 2
+#define USTFWI_ERR_CUDA 3
+#define USTFWI_ERR_OOM 4
+#define USTFWI_ERR_NCCL 5
+
+#define USTFWI_STAGGER_NONE 0  /* Stagger::none  (spectral.hpp:15) */
+#define USTFWI_STAGGER_PLUS 1  /* Stagger::plus  */
+#define USTFWI_STAGGER_MINUS 2 /* Stagger::minus */
+
+/* Field-for-field image of ustfwi::Grid (grid/grid.hpp:14-20); unused axes are 0. */
+typedef struct ustfwi_grid {
+    int ndim;
+    int dims[3];
+    double dx[3];
+    double dt;
+    int nt;
+    int pml_size[3];
+    double c_ref;
+} ustfwi_grid;
+
+USTFWI_API const char* ustfwi_last_error(void);
+USTFWI_API const char* ustfwi_version(void);
+
+/* ------------------------------------------------------------------------------------
+ * Host-side setup (C++ in the library; no device needed)
+ * ------------------------------------------------------------------------------------ */
+
+/* Grid::validate (grid.hpp:35-51). */
+USTFWI_API int ustfwi_grid_validate(const ustfwi_grid* grid);
+/* choose_pml_size (grid.hpp:70-86). */
+USTFWI_API int ustfwi_choose_pml_size(int ndim, const int* interior, int* pml_out);
+/* make_grid (grid.hpp:91-103). */
+USTFWI_API int ustfwi_make_grid(int ndim, const int* interior, double dx, double c_max, double duration,
+                     double cfl, ustfwi_grid* out);
+/* make_pml (grid.hpp:153-178): regular/staggered are concatenated per axis (sum of dims). */
+USTFWI_API int ustfwi_make_pml(const ustfwi_grid* grid, double alpha, double* regular, double* staggered);
+/* shell_indices (solver/medium.hpp:168-178) with erode (:137-165). Two-call protocol:
+ * out == NULL queries *count; otherwise writes min(*count, n) indices, sets *count = n. */
+USTFWI_API int ustfwi_shell_indices(int ndim, const int* dims, const uint8_t* mask, int thickness,
+                         size_t* out, size_t* count);
+/* ball_mask (solver/medium.hpp:181-198). */
+USTFWI_API int ustfwi_ball_mask(int ndim, const int* dims, const double* center, double radius_points,
+                     uint8_t* out);
+/* synth_source_pulse (solver/simulate.hpp:124-148); same two-call protocol via *len. */
+USTFWI_API int ustfwi_synth_source_pulse(const ustfwi_grid* grid, double center_freq_fraction, double c0_min,
+                              double* out, int* len);
+/* Encoding realization (SPEC.md stochastic_estimators, EncodingRealization :277-280, RNG
+ * contract :331-334): Rademacher weights w_i in {-1,+1} and delays d_i ~ U[0,1] quantized to
+ * delay_steps_i = round(d_i * tau / dt), from a counter-based stream keyed by
+ * (master_seed, iteration, index). Bit-identical for identical keys. */
+USTFWI_API int ustfwi_draw_realization(size_t n_src, double tau, double dt, uint64_t master_seed,
+                            uint64_t iteration, uint64_t index, int8_t* weights,
+                            int32_t* delay_steps, double* delays_unit);
+
+/* ------------------------------------------------------------------------------------
+ * Device engine
+ * ------------------------------------------------------------------------------------ */
+typedef struct ustfwi_gpu_ctx ustfwi_gpu_ctx;
+
+/* SpectralEngine(grid) (engine.hpp:19-79): validates the grid, builds the per-axis FFT
+ * plans / wavenumber and stagger tables on `device`, allocates state for two steppers. */
+USTFWI_API int ustfwi_gpu_create(int device, const ustfwi_grid* grid, ustfwi_gpu_ctx** out);
+USTFWI_API void ustfwi_gpu_destroy(ustfwi_gpu_ctx* ctx);
+
+/* Medium (solver/medium.hpp:26-58) + the per-medium part of the WaveStepper constructor
+ * (engine.hpp:184-259): CFL guard (NumericalError), c0^2, dt*rho0, dt/rho0 staggered via
+ * fourier_shift. alpha0 may be NULL (lossless); gamma may be NULL. Absorbing media
+ * (alpha0 != 0) are rejected with USTFWI_ERR_INVALID in this version. */
+USTFWI_API int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* ctx, const double* c0, const double* rho0,
+                          const double* alpha0, double y, const uint8_t* gamma, double c0_min,
+                          double c0_max);
+
+/* SourceSet (solver/medium.hpp:74-85), generalised to encoded super-sources: source i fires
+ * at flat index pos[i] with sample(i, n) = w_i * sig[sig_off[i] + n - delay_i] when
+ * 0 <= n - delay_i < sig_off[i+1] - sig_off[i], else 0. weights / delay_steps may be NULL
+ * (w = 1, delay = 0): the plain reference SourceSet. */
+USTFWI_API int ustfwi_gpu_set_sources(ustfwi_gpu_ctx* ctx, size_t n_src, const size_t* pos,
+                           const size_t* sig_off, const double* sig, const double* weights,
+                           const int32_t* delay_steps);
+/* SensorArray (solver/medium.hpp:88-91). */
+USTFWI_API int ustfwi_gpu_set_sensors(ustfwi_gpu_ctx* ctx, size_t n_sensors, const size_t* pos);
+
+/* simulate_forward (solver/simulate.hpp:30-105). data_out: [n_sensors * nt] sensor-major
+ * (SensorData, medium.hpp:94-114). If boundary_thickness > 0 the shell trace
+ * (BoundaryTrace, medium.hpp:118-133) is recorded; trace_out (nullable) receives
+ * [nt * n_shell] step-major and *n_shell_out the shell size. */
+USTFWI_API int ustfwi_gpu_forward(ustfwi_gpu_ctx* ctx, int boundary_thickness, double* data_out,
+                       double* trace_out, size_t* n_shell_out);
+
+/* gradient_time_reversal / compute_gradient TR branch (adjoint/gradient.hpp:333-464,478-488)
+ * for GradientParam::c0: forward with shell record, adjoint source (reverse, Kahan loss,
+ * cumsum; :264-289), interleaved adjoint + time-reversal replay with in-kernel c0
+ * correlation, gradient zeroed outside gamma. observed: [n_sensors * nt] sensor-major. */
+USTFWI_API int ustfwi_gpu_gradient_tr(ustfwi_gpu_ctx* ctx, const double* observed, int boundary_thickness,
+                           double* grad_out, double* loss_out);
+
+/* evaluate_loss (adjoint/gradient.hpp:491-505). */
+USTFWI_API int ustfwi_gpu_evaluate_loss(ustfwi_gpu_ctx* ctx, const double* observed, double* loss_out);
+
+/* SpectralEngine::derivative (engine.hpp:118-121): out = d/dx_axis f on the grid staggered
+ * by stagger (USTFWI_STAGGER_*). Test/diagnostic entry of the K1 passes. */
+USTFWI_API int ustfwi_gpu_derivative(ustfwi_gpu_ctx* ctx, const double* f, int axis, int stagger,
+                          double* out);
+
+/* ---- device-resident variants (inputs already in HBM; used by the benchmark and by the
+ *      multi-GPU mini-batch driver) ---- */
+USTFWI_API int ustfwi_gpu_upload_observed(ustfwi_gpu_ctx* ctx, const double* observed);
+/* One TR gradient from the uploaded observed data; the result stays on the device and is
+ * ADDED to the context's mini-batch accumulator when accumulate != 0 (else replaces it). */
+USTFWI_API int ustfwi_gpu_run_gradient(ustfwi_gpu_ctx* ctx, int boundary_thickness, int accumulate);
+/* Copy the accumulator (gradient and loss, divided by `scale_div` >= 1) to the host. */
+USTFWI_API int ustfwi_gpu_download_gradient(ustfwi_gpu_ctx* ctx, double scale_div, double* grad_out,
+                                 double* loss_out);
+/* Device pointer of the fp32 gradient accumulator (N floats) and its loss (1 double). */
+USTFWI_API int ustfwi_gpu_accumulator(ustfwi_gpu_ctx* ctx, float** grad_dev, double** loss_dev);
+USTFWI_API int ustfwi_gpu_synchronize(ustfwi_gpu_ctx* ctx);
+/* Stream the engine launches on (cudaStream_t as void*). */
+USTFWI_API void* ustfwi_gpu_stream(ustfwi_gpu_ctx* ctx);
+/* Number of kernel launches issued by this context since creation. */
+USTFWI_API uint64_t ustfwi_gpu_launch_count(const ustfwi_gpu_ctx* ctx);
+/* Shell size of the last forward with boundary recording. */
+USTFWI_API size_t ustfwi_gpu_shell_size(const ustfwi_gpu_ctx* ctx);
+
+/* ---- per-launch-class device timing (CUDA events on the engine stream) ---- */
+#define USTFWI_KERNEL_Y 0    /* y-pencil FFT passes */
+#define USTFWI_KERNEL_X 1    /* x-pencil FFT * kappa * D_x * IFFT passes */
+#define USTFWI_KERNEL_ZVEL 2 /* fused z c2r + velocity update + r2c */
+#define USTFWI_KERNEL_ZRHO 3 /* fused z c2r + density/pressure/sparse/correlation + r2c */
+#define USTFWI_KERNEL_AUX 4
+#define USTFWI_KERNEL_KINDS 5
+/* Enable/disable event timing of every launch and reset the counters. */
+USTFWI_API int ustfwi_gpu_set_profiling(ustfwi_gpu_ctx* ctx, int enable);
+/* Accumulated device time, launch count and algorithmic bytes (minimum HBM traffic of the
+ * launches: half-spectrum and field reads + writes) of one launch class. */
+USTFWI_API int ustfwi_gpu_kernel_stats(ustfwi_gpu_ctx* ctx, int kind, double* total_ms,
+                                       uint64_t* launches, double* bytes);
+
+/* ---- mini-batch mean over GPUs (SPEC.md average_estimates :314-322; PAPER §4.5) ---- */
+/* ncclGetUniqueId into 128 bytes. */
+USTFWI_API int ustfwi_nccl_unique_id(char id_out[128]);
+/* Bind an NCCL communicator (one rank per GPU) to the context. */
+USTFWI_API int ustfwi_gpu_comm_init(ustfwi_gpu_ctx* ctx, const char id[128], int nranks, int rank);
+/* In place: accumulator <- (sum over ranks of accumulator) / batch, loss likewise. */
+USTFWI_API int ustfwi_gpu_allreduce_mean(ustfwi_gpu_ctx* ctx, int batch);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* USTFWI_CAPI_H */

@@ -1,0 +1,1091 @@
+// Device engine: context (the device analogue of SpectralEngine + WaveSteppers,
+// engine.hpp:17-386), the forward simulation (simulate.hpp:30-105) and the time-reversal
+// c0 gradient (gradient.hpp:333-464) orchestrated as fused pass launches on one stream,
+// and the device half of the C ABI (include/ustfwi_capi.h).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "host_setup.hpp"
+#include "kernels.cuh"
+
+using namespace ustfwi_dev;
+using ustfwi_host::Error;
+using ustfwi_host::fail;
+
+namespace {
+
+#define CK(expr)                                                                               \
+    do {                                                                                       \
+        cudaError_t e_ = (expr);                                                               \
+        if (e_ != cudaSuccess)                                                                 \
+            fail(e_ == cudaErrorMemoryAllocation ? USTFWI_ERR_OOM : USTFWI_ERR_CUDA,           \
+                 std::string(#expr) + ": " + cudaGetErrorString(e_));                          \
+    } while (0)
+
+enum { ST_NONE = 0, ST_PLUS = 1, ST_MINUS = 2, ST_SHIFT = 3 };
+enum { KIND_Y = 0, KIND_X = 1, KIND_ZVEL = 2, KIND_ZRHO = 3, KIND_AUX = 4 };
+
+struct Sim {
+    float* p = nullptr;
+    float* v[3] = {};
+    float* rho[3] = {};
+    float2* S[3] = {};
+};
+
+// Device image of a SourceSet: unique positions (sorted) + CSR of contributions.
+struct InjectSet {
+    int n_unique = 0;
+    std::vector<int> h_pos;            // unique positions
+    int* pos = nullptr;
+    int* csr = nullptr;
+    int* off = nullptr;
+    int* len = nullptr;
+    int* stride = nullptr;
+    int* delay = nullptr;
+    float* w = nullptr;
+    float* sig = nullptr;              // owned signal table (sources) or borrowed (adjoint q)
+    float* scale = nullptr;
+    SparseInject view(const float* sig_override = nullptr) const {
+        SparseInject s;
+        s.n_unique = n_unique;
+        s.pos = pos;
+        s.csr = csr;
+        s.off = off;
+        s.len = len;
+        s.stride = stride;
+        s.delay = delay;
+        s.w = w;
+        s.sig = sig_override ? sig_override : sig;
+        s.scale = scale;
+        return s;
+    }
+};
+
+// NCCL, resolved lazily with dlopen so the library has no link-time NCCL dependency
+// (and shares whichever libnccl.so.2 the process already loaded, e.g. torch's).
+struct NcclApi {
+    void* h = nullptr;
+    int (*get_unique_id)(void*) = nullptr;
+    int (*comm_init_rank)(void**, int, const void*, int) = nullptr;  // ncclUniqueId passed by value (128 B)
+    int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*comm_destroy)(void*) = nullptr;
+    const char* (*error_string)(int) = nullptr;
+};
+struct NcclUniqueId {
+    char internal[128];
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    if (!api.h) {
+        api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!api.h) fail(USTFWI_ERR_NCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
+        api.get_unique_id = reinterpret_cast<int (*)(void*)>(dlsym(api.h, "ncclGetUniqueId"));
+        api.all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+            dlsym(api.h, "ncclAllReduce"));
+        api.comm_destroy = reinterpret_cast<int (*)(void*)>(dlsym(api.h, "ncclCommDestroy"));
+        api.error_string = reinterpret_cast<const char* (*)(int)>(dlsym(api.h, "ncclGetErrorString"));
+        if (!api.get_unique_id || !api.all_reduce || !api.comm_destroy)
+            fail(USTFWI_ERR_NCCL, "libnccl.so.2 lacks the expected symbols");
+    }
+    return api;
+}
+
+}  // namespace
+
+struct ustfwi_gpu_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t launches = 0;
+    ustfwi_grid grid{};
+    int ndim = 3;
+    int off_axis = 0;   // 3 - ndim: padded axis of reference axis 0
+    GridDev g{};
+    std::vector<void*> allocs;
+
+    float2* dmul[3][4] = {};  // per padded axis: none / plus / minus / shift tables
+    float* pml_reg[3] = {};
+    float* pml_stag[3] = {};
+
+    // medium
+    bool has_medium = false;
+    float* c0sq = nullptr;
+    Coef dtrho0{};
+    Coef dtr_stag[3]{};
+    float* dtr_fields = nullptr;   // 4 fields when rho0 is not uniform
+    uint8_t* gamma = nullptr;
+    std::vector<uint8_t> gamma_host;
+    std::vector<double> c0_host;
+
+    Sim sim[2];
+    float* ring[3] = {};
+    float* grad = nullptr;
+    float* acc = nullptr;
+    double* loss = nullptr;       // [0] last loss, [1] accumulated loss
+    int* flags = nullptr;         // [0] diverged step (INT_MAX = ok), [1] nonfinite grad, [2] nonfinite data
+
+    // sources / sensors / data
+    InjectSet src, adj;
+    std::vector<size_t> src_pos_host;
+    int n_sens = 0;
+    std::vector<size_t> sens_pos_host;
+    int* sens_pos = nullptr;   // sorted
+    int* sens_idx = nullptr;
+    float* data = nullptr;     // [nt][ns]
+    double* obs = nullptr;     // [nt][ns]
+    float* q = nullptr;        // [nt][ns]
+    double* loss_part = nullptr;
+    bool obs_ready = false;
+
+    // shell
+    int shell_thickness = 0;
+    std::vector<size_t> shell_host;
+    int* shell_pos = nullptr;
+    float* trace = nullptr;
+    size_t trace_elems = 0;
+
+    void* comm = nullptr;
+
+    // per-launch-class CUDA-event timing (ustfwi_gpu_set_profiling / ustfwi_gpu_kernel_stats)
+    struct Pending {
+        cudaEvent_t a, b;
+        int kind;
+        double bytes;
+    };
+    bool profiling = false;
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+    double prof_ms[USTFWI_KERNEL_KINDS] = {};
+    double prof_bytes[USTFWI_KERNEL_KINDS] = {};
+    uint64_t prof_n[USTFWI_KERNEL_KINDS] = {};
+
+    cudaEvent_t get_event() {
+        if (event_pool.empty()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            return e;
+        }
+        cudaEvent_t e = event_pool.back();
+        event_pool.pop_back();
+        return e;
+    }
+    template <class F>
+    void launch(int kind, double bytes, F&& f) {
+        if (!profiling) {
+            count(f());
+            return;
+        }
+        Pending pd{get_event(), get_event(), kind, bytes};
+        CK(cudaEventRecord(pd.a, stream));
+        count(f());
+        CK(cudaEventRecord(pd.b, stream));
+        pending.push_back(pd);
+        if (pending.size() > 4096) resolve_profile();
+    }
+    void resolve_profile() {
+        for (auto& pd : pending) {
+            CK(cudaEventSynchronize(pd.b));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, pd.a, pd.b));
+            prof_ms[pd.kind] += ms;
+            prof_bytes[pd.kind] += pd.bytes;
+            prof_n[pd.kind] += 1;
+            event_pool.push_back(pd.a);
+            event_pool.push_back(pd.b);
+        }
+        pending.clear();
+    }
+
+    template <class T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+        allocs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    void release(void* p) {
+        if (!p) return;
+        auto it = std::find(allocs.begin(), allocs.end(), p);
+        if (it != allocs.end()) {
+            cudaFree(p);
+            allocs.erase(it);
+        }
+    }
+    template <class T>
+    T* upload(const std::vector<T>& h) {
+        T* d = alloc<T>(h.size());
+        if (!h.empty()) CK(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, stream));
+        return d;
+    }
+    void count(cudaError_t e) {
+        if (e != cudaSuccess) fail(USTFWI_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+        ++launches;
+    }
+};
+
+namespace {
+
+using Ctx = ustfwi_gpu_ctx;
+
+FftPlan make_plan(Ctx& c, int L) {
+    FftPlan p{};
+    p.L = L;
+    int m = L;
+    auto take = [&](int r) {
+        while (m % r == 0 && p.nstages < kMaxStages) {
+            p.radix[p.nstages++] = r;
+            m /= r;
+        }
+    };
+    take(16);
+    take(8);
+    take(4);
+    take(2);
+    take(5);
+    take(3);
+    take(7);
+    for (int f = 11; m > 1 && p.nstages < kMaxStages; f += 2) take(f);
+    if (m != 1) fail(USTFWI_ERR_INVALID, "transform length " + std::to_string(L) + " has too many factors");
+    std::vector<float2> tw(static_cast<size_t>(L));
+    for (int k = 0; k < L; ++k) {
+        const double a = -2.0 * M_PI * static_cast<double>(k) / static_cast<double>(L);
+        tw[static_cast<size_t>(k)] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+    }
+    p.tw = c.upload(tw);
+    return p;
+}
+
+long long rows_of(const Ctx& c) { return c.g.rows; }
+
+void reset_sim(Ctx& c, Sim& s, bool with_p) {
+    const size_t nb = static_cast<size_t>(c.g.N) * sizeof(float);
+    const size_t sb = static_cast<size_t>(rows_of(c)) * c.g.nzp * sizeof(float2);
+    for (int a = 0; a < 3; ++a) {
+        CK(cudaMemsetAsync(s.v[a], 0, nb, c.stream));
+        CK(cudaMemsetAsync(s.rho[a], 0, nb, c.stream));
+    }
+    CK(cudaMemsetAsync(s.S[0], 0, sb, c.stream));
+    if (with_p && s.p) CK(cudaMemsetAsync(s.p, 0, nb, c.stream));
+}
+
+struct StepIO {
+    SparseInject inj{};
+    SparseEnforce enf{};
+    SparseGather sens{};
+    SparseGather shell{};
+    Correlate corr{};
+    int step_n = 0;
+    int check_step = 0;
+    float* p_out = nullptr;
+};
+
+// One leapfrog step of a stepper: update_velocity_density (engine.hpp:270-292), sparse
+// injection / shell enforcement, update_pressure (:318-347), gathers — 8 launches.
+void run_step(Ctx& c, Sim& s, const StepIO& io) {
+    const GridDev& g = c.g;
+    const double SB = static_cast<double>(g.rows) * g.nzh * sizeof(float2);  // one half spectrum
+    const double FB = static_cast<double>(g.N) * sizeof(float);               // one real field
+    auto pencil = [&](int axis, bool inv, const PencilJobs& j) {
+        int loads = 0;
+        for (int q = 0; q < j.n; ++q)
+            if (q == 0 || j.job[q].src != j.job[q - 1].src) ++loads;
+        c.launch(axis == 0 ? KIND_X : KIND_Y, (loads + j.n) * SB,
+                 [&] { return launch_pencil(axis, inv, g, j, c.stream); });
+    };
+    PencilJobs j{};
+    for (int f = 0; f < 3; ++f) j.buf[f] = s.S[f];
+    // Y forward of Fz p
+    j.n = 1;
+    j.job[0] = {0, 0, nullptr, 0};
+    pencil(1, false, j);
+    // X: (kappa D_x+ , kappa)
+    j.n = 2;
+    j.job[0] = {0, 0, c.dmul[0][ST_PLUS], 1};
+    j.job[1] = {0, 1, nullptr, 1};
+    pencil(0, false, j);
+    // Y inverse: S0 <- T_x, S2 <- T_kappa, S1 <- D_y+ T_kappa
+    j.n = 3;
+    j.job[0] = {0, 0, nullptr, 0};
+    j.job[1] = {1, 2, nullptr, 0};
+    j.job[2] = {1, 1, c.dmul[1][ST_PLUS], 0};
+    pencil(1, true, j);
+    // Z: c2r (D_z+ on S2), velocity update, r2c of v
+    Pml ps{{c.pml_stag[0], c.pml_stag[1], c.pml_stag[2]}};
+    const double coef_b = c.dtr_stag[0].field ? 3 * FB : 0.0;
+    c.launch(KIND_ZVEL, 6 * SB + 6 * FB + coef_b,
+             [&] { return launch_zvel(g, s.S, c.dmul[2][ST_PLUS], s.v, ps, c.dtr_stag, c.stream); });
+    // Y forward x3
+    j.n = 3;
+    for (int f = 0; f < 3; ++f) j.job[f] = {f, f, nullptr, 0};
+    pencil(1, false, j);
+    // X: kappa D_x-, kappa, kappa
+    j.job[0] = {0, 0, c.dmul[0][ST_MINUS], 1};
+    j.job[1] = {1, 1, nullptr, 1};
+    j.job[2] = {2, 2, nullptr, 1};
+    pencil(0, false, j);
+    // Y inverse x3 (D_y- on S1)
+    j.job[0] = {0, 0, nullptr, 0};
+    j.job[1] = {1, 1, c.dmul[1][ST_MINUS], 0};
+    j.job[2] = {2, 2, nullptr, 0};
+    pencil(1, true, j);
+    // Z: c2r (D_z- on S2), density update, sparse ops, pressure, gathers, Fz p
+    ZrhoArgs a{};
+    for (int f = 0; f < 3; ++f) {
+        a.S[f] = s.S[f];
+        a.rho[f] = s.rho[f];
+    }
+    a.dz_minus = c.dmul[2][ST_MINUS];
+    a.pml = Pml{{c.pml_reg[0], c.pml_reg[1], c.pml_reg[2]}};
+    a.dtrho0 = c.dtrho0;
+    a.c0sq = c.c0sq;
+    a.p_out = io.p_out;
+    a.a_first = c.off_axis;
+    a.step_n = io.step_n;
+    a.inj = io.inj;
+    a.enf = io.enf;
+    a.sens = io.sens;
+    a.shell = io.shell;
+    a.corr = io.corr;
+    a.check_step = io.check_step;
+    a.diverged = c.flags;
+    const double zb = 4 * SB + 8 * FB + (c.dtrho0.field ? FB : 0.0) + (io.corr.grad ? 5 * FB : 0.0);
+    c.launch(KIND_ZRHO, zb, [&] { return launch_zrho(g, a, true, c.stream); });
+}
+
+// Build the device InjectSet for `n` contributions at flat positions pos[i].
+void build_inject(Ctx& c, InjectSet& set, const std::vector<size_t>& pos, const std::vector<int>& off,
+                  const std::vector<int>& len, const std::vector<int>& stride, const std::vector<int>& delay,
+                  const std::vector<float>& w) {
+    for (void* p : {(void*)set.pos, (void*)set.csr, (void*)set.off, (void*)set.len, (void*)set.stride,
+                    (void*)set.delay, (void*)set.w, (void*)set.scale})
+        c.release(p);
+    const size_t n = pos.size();
+    std::vector<size_t> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return pos[a] < pos[b]; });
+    std::vector<int> upos, csr{0}, o, l, st, d;
+    std::vector<float> ww;
+    for (size_t k = 0; k < n; ++k) {
+        const size_t i = order[k];
+        if (upos.empty() || static_cast<size_t>(upos.back()) != pos[i]) {
+            if (!upos.empty()) csr.push_back(static_cast<int>(o.size()));
+            upos.push_back(static_cast<int>(pos[i]));
+        }
+        o.push_back(off[i]);
+        l.push_back(len[i]);
+        st.push_back(stride[i]);
+        d.push_back(delay[i]);
+        ww.push_back(w[i]);
+    }
+    if (!upos.empty()) csr.push_back(static_cast<int>(o.size()));
+    set.n_unique = static_cast<int>(upos.size());
+    set.h_pos = upos;
+    set.pos = c.upload(upos);
+    set.csr = c.upload(csr);
+    set.off = c.upload(o);
+    set.len = c.upload(l);
+    set.stride = c.upload(st);
+    set.delay = c.upload(d);
+    set.w = c.upload(ww);
+    set.scale = c.alloc<float>(upos.size());
+}
+
+// inject_mass_source scale 2*dt/(ndim*dx*c0(x)) (engine.hpp:296-300), from the current medium.
+void refresh_scales(Ctx& c, InjectSet& set) {
+    std::vector<float> sc(set.h_pos.size());
+    for (size_t u = 0; u < sc.size(); ++u) {
+        const double c0 = c.c0_host[static_cast<size_t>(set.h_pos[u])];
+        sc[u] = static_cast<float>(2.0 * c.grid.dt / (c.ndim * c.grid.dx[0] * std::sqrt(c0 * c0)));
+    }
+    if (!sc.empty())
+        CK(cudaMemcpyAsync(set.scale, sc.data(), sc.size() * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+}
+
+void require_medium(const Ctx& c) {
+    if (!c.has_medium) fail(USTFWI_ERR_INVALID, "medium not set (ustfwi_gpu_set_medium)");
+}
+
+void ensure_data_buffers(Ctx& c) {
+    if (c.data) return;
+    const size_t n = static_cast<size_t>(c.grid.nt) * std::max(c.n_sens, 1);
+    c.data = c.alloc<float>(n);
+    c.obs = c.alloc<double>(n);
+    c.q = c.alloc<float>(n);
+    c.loss_part = c.alloc<double>(std::max(c.n_sens, 1));
+}
+
+void prepare_shell(Ctx& c, int thickness) {
+    if (c.gamma_host.empty()) fail(USTFWI_ERR_INVALID, "boundary recording requires a gamma mask");
+    if (thickness != c.shell_thickness || !c.shell_pos) {
+        c.release(c.shell_pos);
+        c.shell_pos = nullptr;
+        std::vector<int> dims(c.grid.dims, c.grid.dims + c.grid.ndim);
+        c.shell_host = ustfwi_host::shell_indices(c.gamma_host, dims, thickness);
+        std::vector<int> sp(c.shell_host.begin(), c.shell_host.end());
+        c.shell_pos = c.upload(sp);
+        c.shell_thickness = thickness;
+    }
+    const size_t need = c.shell_host.size() * static_cast<size_t>(c.grid.nt);
+    if (need > c.trace_elems) {
+        c.release(c.trace);
+        c.trace = c.alloc<float>(need);
+        c.trace_elems = need;
+    }
+}
+
+void clear_flags(Ctx& c) {
+    const int init[3] = {INT_MAX, 0, 0};
+    CK(cudaMemcpyAsync(c.flags, init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
+}
+
+void check_flags(Ctx& c, bool grad_phase) {
+    int f[3];
+    CK(cudaMemcpyAsync(f, c.flags, sizeof(f), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    c.resolve_profile();
+    if (f[0] != INT_MAX) fail(USTFWI_ERR_NUMERICAL, "pressure field diverged at step " + std::to_string(f[0]));
+    if (f[2]) fail(USTFWI_ERR_NUMERICAL, "sensor data contains non-finite values");
+    if (grad_phase && f[1]) fail(USTFWI_ERR_NUMERICAL, "gradient contains non-finite values");
+}
+
+// simulate_forward (simulate.hpp:76-103): nt steps of stepper 0 with the source set,
+// sensor gather into c.data ([nt][ns]) and optional shell record into c.trace.
+void forward_sim(Ctx& c, int thickness) {
+    require_medium(c);
+    ensure_data_buffers(c);
+    if (thickness > 0) prepare_shell(c, thickness);
+    refresh_scales(c, c.src);
+    Sim& s = c.sim[0];
+    reset_sim(c, s, true);
+    const int nt = c.grid.nt;
+    const int n_shell = thickness > 0 ? static_cast<int>(c.shell_host.size()) : 0;
+    StepIO io;
+    io.inj = c.src.view();
+    io.sens = SparseGather{c.n_sens, c.sens_pos, c.sens_idx, nullptr};
+    io.shell = SparseGather{n_shell, c.shell_pos, nullptr, nullptr};
+    io.p_out = s.p;
+    for (int n = 0; n < nt; ++n) {
+        io.step_n = n;
+        io.sens.out = c.data + static_cast<size_t>(n) * c.n_sens;
+        if (n_shell) io.shell.out = c.trace + static_cast<size_t>(n) * n_shell;
+        io.check_step = ((n + 1) & 63) == 0 ? n + 1 : 0;
+        run_step(c, s, io);
+    }
+    if (c.n_sens > 0) c.count(launch_check_finite(c.data, static_cast<long long>(nt) * c.n_sens, c.flags + 2, c.stream));
+}
+
+// compute_gradient, TR branch (gradient.hpp:359-462), GradientParam::c0.
+void gradient_tr(Ctx& c, int thickness, bool accumulate) {
+    require_medium(c);
+    if (c.gamma_host.empty()) fail(USTFWI_ERR_INVALID, "gradient computation requires a gamma mask");
+    if (!c.obs_ready) fail(USTFWI_ERR_INVALID, "observed data not uploaded");
+    if (thickness < 1) fail(USTFWI_ERR_INVALID, "shell thickness must be >= 1");
+    const int nt = c.grid.nt, ns = c.n_sens, last = nt - 1;
+    forward_sim(c, thickness);
+    // adjoint source: reverse, Kahan loss, integrate (gradient.hpp:264-289,378-379)
+    c.count(launch_adjoint_source(c.data, c.obs, nt, ns, 1, c.q, c.loss_part, c.loss, c.loss + 1,
+                                  accumulate ? 1 : 0, c.stream));
+    c.launches += 1;  // loss reduction kernel
+    refresh_scales(c, c.adj);
+    Sim& adj = c.sim[0];
+    Sim& rep = c.sim[1];
+    reset_sim(c, adj, true);
+    reset_sim(c, rep, false);
+    CK(cudaMemsetAsync(c.grad, 0, static_cast<size_t>(c.g.N) * sizeof(float), c.stream));
+    const int n_shell = static_cast<int>(c.shell_host.size());
+    auto shell_row = [&](int m) { return c.trace + static_cast<size_t>(m) * n_shell; };
+
+    // replay initial value: enforce g[last], refresh p (gradient.hpp:435-437)
+    {
+        ZrhoArgs a{};
+        for (int f = 0; f < 3; ++f) {
+            a.S[f] = rep.S[f];
+            a.rho[f] = rep.rho[f];
+        }
+        a.pml = Pml{{c.pml_reg[0], c.pml_reg[1], c.pml_reg[2]}};
+        a.dtrho0 = c.dtrho0;
+        a.c0sq = c.c0sq;
+        a.p_out = c.ring[0];
+        a.a_first = c.off_axis;
+        a.enf = SparseEnforce{n_shell, c.shell_pos, shell_row(last), static_cast<float>(c.ndim)};
+        a.diverged = c.flags;
+        c.count(launch_zrho(c.g, a, false, c.stream));
+    }
+    // look-ahead step (gradient.hpp:438-441)
+    StepIO rio;
+    rio.enf = SparseEnforce{n_shell, c.shell_pos, shell_row(last - 1), static_cast<float>(c.ndim)};
+    rio.p_out = c.ring[1];
+    rio.check_step = 0;
+    run_step(c, rep, rio);
+
+    StepIO aio;
+    aio.inj = c.adj.view(c.q);
+    aio.p_out = adj.p;
+    const float inv_dt = static_cast<float>(1.0 / c.grid.dt);
+    for (int n = 1; n <= last - 1; ++n) {
+        aio.step_n = n;
+        aio.check_step = (n & 63) == 0 ? n : 0;
+        run_step(c, adj, aio);
+        rio.enf.vals = shell_row(last - n - 1);
+        rio.p_out = c.ring[(n + 1) % 3];
+        rio.corr = Correlate{c.ring[n % 3], c.ring[(n - 1) % 3], adj.p, c.grad, inv_dt};
+        rio.check_step = ((n + 1) & 63) == 0 ? n + 1 : 0;
+        run_step(c, rep, rio);
+    }
+    c.count(launch_finalize_grad(c.grad, c.gamma, c.g.N, c.acc, accumulate ? 1 : 0, c.flags + 1, c.stream));
+}
+
+template <class Fn>
+int guarded(Ctx* c, Fn&& fn) {
+    try {
+        if (c) CK(cudaSetDevice(c->device));
+        fn();
+        return USTFWI_OK;
+    } catch (const Error& e) {
+        ustfwi_host::set_last_error(e.msg);
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        ustfwi_host::set_last_error("host allocation failed");
+        return USTFWI_ERR_OOM;
+    } catch (const std::exception& e) {
+        ustfwi_host::set_last_error(e.what());
+        return USTFWI_ERR_INVALID;
+    }
+}
+
+std::vector<float> to_f32(const double* p, size_t n) {
+    std::vector<float> out(n);
+    for (size_t i = 0; i < n; ++i) out[i] = static_cast<float>(p[i]);
+    return out;
+}
+
+// fourier_shift(rho0, axis, +1/2) (spectral.hpp:94-112) on the device: the multiplier
+// depends on k_axis only, applied inside the pass of that axis.
+void staggered_shift(Ctx& c, const float* src, int axis, float* out) {
+    Sim& s = c.sim[1];
+    c.count(launch_zfwd(c.g, src, s.S[0], c.stream));
+    PencilJobs j{};
+    for (int f = 0; f < 3; ++f) j.buf[f] = s.S[f];
+    j.n = 1;
+    j.job[0] = {0, 0, nullptr, 0};
+    c.count(launch_pencil(1, false, c.g, j, c.stream));
+    j.job[0] = {0, 0, axis == 0 ? c.dmul[0][ST_SHIFT] : nullptr, 0};
+    // X pass always multiplies through a job; kappa off
+    c.count(launch_pencil(0, false, c.g, j, c.stream));
+    j.job[0] = {0, 0, axis == 1 ? c.dmul[1][ST_SHIFT] : nullptr, 0};
+    c.count(launch_pencil(1, true, c.g, j, c.stream));
+    c.count(launch_zinv(c.g, s.S[0], axis == 2 ? c.dmul[2][ST_SHIFT] : nullptr, out, c.stream));
+}
+
+}  // namespace
+
+// =====================================================================================
+// C ABI: device engine
+// =====================================================================================
+extern "C" {
+
+int ustfwi_gpu_create(int device, const ustfwi_grid* grid, ustfwi_gpu_ctx** out) {
+    *out = nullptr;
+    auto* c = new (std::nothrow) Ctx;
+    if (!c) return USTFWI_ERR_OOM;
+    const int rc = guarded(nullptr, [&] {
+        if (!grid) fail(USTFWI_ERR_INVALID, "null grid");
+        ustfwi_host::validate_grid(*grid);
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            fail(USTFWI_ERR_CUDA, "no CUDA device available (the engine has no CPU fallback)");
+        if (device < 0 || device >= ndev) fail(USTFWI_ERR_INVALID, "device index out of range");
+        c->device = device;
+        CK(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10)
+            fail(USTFWI_ERR_CUDA, std::string("device ") + prop.name + " is not sm_100-class (built for sm_100a)");
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->grid = *grid;
+        c->ndim = grid->ndim;
+        c->off_axis = 3 - grid->ndim;
+        int d3[3] = {1, 1, 1};
+        double dx3[3] = {grid->dx[0], grid->dx[0], grid->dx[0]};
+        for (int a = 0; a < grid->ndim; ++a) {
+            d3[c->off_axis + a] = grid->dims[a];
+            dx3[c->off_axis + a] = grid->dx[a];
+        }
+        GridDev& g = c->g;
+        g.nx = d3[0];
+        g.ny = d3[1];
+        g.nz = d3[2];
+        g.nzh = g.nz / 2 + 1;
+        g.nzp = (g.nzh + 3) & ~3;
+        g.rows = static_cast<long long>(g.nx) * g.ny;
+        g.N = g.rows * g.nz;
+        if (g.N >= (1LL << 31)) fail(USTFWI_ERR_INVALID, "grid larger than 2^31 points is not supported");
+        g.px = make_plan(*c, g.nx);
+        g.py = make_plan(*c, g.ny);
+        g.pzh = make_plan(*c, g.nz / 2);
+        std::vector<float2> twr(static_cast<size_t>(g.nzh));
+        for (int k = 0; k < g.nzh; ++k) {
+            const double a = -2.0 * M_PI * k / g.nz;
+            twr[static_cast<size_t>(k)] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+        }
+        g.tw_rfft = c->upload(twr);
+        g.half_cdt = static_cast<float>(0.5 * grid->c_ref * grid->dt);
+        g.inv_n = static_cast<float>(1.0 / static_cast<double>(g.N));
+        // per-axis wavenumbers, stagger/shift factors (engine.hpp:46-78) and PML (grid.hpp:153-178)
+        float* kdev[3];
+        ustfwi_grid g3{};
+        g3.ndim = 3;
+        for (int a = 0; a < 3; ++a) {
+            g3.dims[a] = d3[a];
+            g3.dx[a] = dx3[a];
+            g3.pml_size[a] = 0;
+        }
+        for (int a = 0; a < grid->ndim; ++a) g3.pml_size[c->off_axis + a] = grid->pml_size[a];
+        g3.dt = grid->dt;
+        g3.nt = grid->nt;
+        g3.c_ref = grid->c_ref;
+        for (int a = 0; a < 3; ++a) {
+            const int n = d3[a];
+            const auto k = ustfwi_host::wavenumbers(n, dx3[a]);
+            std::vector<float> kf(k.begin(), k.end());
+            kdev[a] = c->upload(kf);
+            std::vector<float2> tab[4];
+            for (auto& t : tab) t.resize(static_cast<size_t>(n));
+            for (int m = 0; m < n; ++m) {
+                const double km = k[static_cast<size_t>(m)];
+                const double h = 0.5 * km * dx3[a];
+                const bool nyq = (m == n / 2);
+                // i*k, i*k*e^{+ikdx/2}, i*k*e^{-ikdx/2}, e^{+ikdx/2}; real part only on the Nyquist bin
+                tab[ST_NONE][m] = nyq ? make_float2(0.f, 0.f) : make_float2(0.f, static_cast<float>(km));
+                tab[ST_PLUS][m] = make_float2(static_cast<float>(-km * std::sin(h)),
+                                              nyq ? 0.f : static_cast<float>(km * std::cos(h)));
+                tab[ST_MINUS][m] = make_float2(static_cast<float>(km * std::sin(h)),
+                                               nyq ? 0.f : static_cast<float>(km * std::cos(h)));
+                tab[ST_SHIFT][m] = make_float2(static_cast<float>(std::cos(h)), nyq ? 0.f : static_cast<float>(std::sin(h)));
+            }
+            for (int s = 0; s < 4; ++s) c->dmul[a][s] = c->upload(tab[s]);
+            std::vector<double> r, st;
+            if (g3.pml_size[a] > 0) {
+                ustfwi_host::pml_profiles(g3, a, 2.0, r, st);
+            } else {
+                r.assign(static_cast<size_t>(n), 1.0);
+                st.assign(static_cast<size_t>(n), 1.0);
+            }
+            c->pml_reg[a] = c->upload(std::vector<float>(r.begin(), r.end()));
+            c->pml_stag[a] = c->upload(std::vector<float>(st.begin(), st.end()));
+        }
+        g.kx = kdev[0];
+        g.ky = kdev[1];
+        g.kz = kdev[2];
+        // state of two steppers, the replay ring, gradient and accumulator
+        const size_t N = static_cast<size_t>(g.N);
+        const size_t NS = static_cast<size_t>(g.rows) * g.nzp;
+        for (int s = 0; s < 2; ++s) {
+            for (int a = 0; a < 3; ++a) {
+                c->sim[s].v[a] = c->alloc<float>(N);
+                c->sim[s].rho[a] = c->alloc<float>(N);
+                c->sim[s].S[a] = c->alloc<float2>(NS);
+            }
+        }
+        c->sim[0].p = c->alloc<float>(N);
+        for (int r = 0; r < 3; ++r) c->ring[r] = c->alloc<float>(N);
+        c->grad = c->alloc<float>(N);
+        c->acc = c->alloc<float>(N);
+        c->c0sq = c->alloc<float>(N);
+        c->gamma = c->alloc<uint8_t>(N);
+        c->loss = c->alloc<double>(2);
+        c->flags = c->alloc<int>(4);
+        CK(cudaMemsetAsync(c->acc, 0, N * sizeof(float), c->stream));
+        CK(cudaMemsetAsync(c->loss, 0, 2 * sizeof(double), c->stream));
+        clear_flags(*c);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+    if (rc != USTFWI_OK) {
+        ustfwi_gpu_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return USTFWI_OK;
+}
+
+void ustfwi_gpu_destroy(ustfwi_gpu_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm) {
+        try {
+            nccl().comm_destroy(c->comm);
+        } catch (...) {
+        }
+    }
+    for (auto& pd : c->pending) {
+        c->event_pool.push_back(pd.a);
+        c->event_pool.push_back(pd.b);
+    }
+    for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+    for (void* p : c->allocs) cudaFree(p);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho0, const double* alpha0, double y,
+                          const uint8_t* gamma, double c0_min, double c0_max) {
+    return guarded(c, [&] {
+        const size_t N = static_cast<size_t>(c->g.N);
+        if (!c0 || !rho0) fail(USTFWI_ERR_INVALID, "medium fields must match the grid");
+        // Medium::validate (medium.hpp:41-57)
+        bool absorbing = false;
+        double cmax = 0.0;
+        for (size_t i = 0; i < N; ++i) {
+            if (c0[i] < c0_min || c0[i] > c0_max) fail(USTFWI_ERR_INVALID, "c0 outside configured bounds");
+            if (!(rho0[i] > 0.0)) fail(USTFWI_ERR_INVALID, "rho0 must be positive");
+            if (alpha0) {
+                if (alpha0[i] < 0.0) fail(USTFWI_ERR_INVALID, "alpha0 must be non-negative");
+                if (alpha0[i] != 0.0) absorbing = true;
+            }
+            cmax = std::max(cmax, c0[i]);
+        }
+        if (y <= 1.0 || y >= 3.0) fail(USTFWI_ERR_INVALID, "power-law exponent must be in (1,3)");
+        if (absorbing)
+            fail(USTFWI_ERR_INVALID, "absorbing media (alpha0 != 0) are not supported by the device engine yet");
+        // WaveStepper constructor checks (engine.hpp:188-197)
+        for (int a = 1; a < c->grid.ndim; ++a)
+            if (c->grid.dx[a] != c->grid.dx[0])
+                fail(USTFWI_ERR_INVALID, "wave stepper requires uniform grid spacing");
+        double min_dx = c->grid.dx[0];
+        for (int a = 1; a < c->grid.ndim; ++a) min_dx = std::min(min_dx, c->grid.dx[a]);
+        if (cmax * c->grid.dt / min_dx > 2.0 / M_PI * (1.0 + 1e-12))
+            fail(USTFWI_ERR_NUMERICAL, "CFL violation: dt exceeds 2/pi * dx / c_max");
+        const double dt = c->grid.dt;
+        c->c0_host.assign(c0, c0 + N);
+        std::vector<float> c2(N);
+        for (size_t i = 0; i < N; ++i) c2[i] = static_cast<float>(c0[i] * c0[i]);
+        CK(cudaMemcpyAsync(c->c0sq, c2.data(), N * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        bool uniform_rho = true;
+        for (size_t i = 1; i < N && uniform_rho; ++i) uniform_rho = rho0[i] == rho0[0];
+        c->release(c->dtr_fields);
+        c->dtr_fields = nullptr;
+        if (uniform_rho) {
+            // fourier_shift of a constant is the constant: scalar coefficients
+            c->dtrho0 = Coef{nullptr, static_cast<float>(dt * rho0[0])};
+            for (int a = 0; a < 3; ++a) c->dtr_stag[a] = Coef{nullptr, static_cast<float>(dt / rho0[0])};
+        } else {
+            c->dtr_fields = c->alloc<float>(4 * N);
+            std::vector<float> f(N);
+            for (size_t i = 0; i < N; ++i) f[i] = static_cast<float>(dt * rho0[i]);
+            CK(cudaMemcpyAsync(c->dtr_fields, f.data(), N * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+            c->dtrho0 = Coef{c->dtr_fields, 0.f};
+            std::vector<float> r(N);
+            for (size_t i = 0; i < N; ++i) r[i] = static_cast<float>(rho0[i]);
+            float* rdev = c->ring[0];  // scratch
+            CK(cudaMemcpyAsync(rdev, r.data(), N * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+            std::vector<float> shifted(N);
+            for (int a = 0; a < 3; ++a) {
+                float* dst = c->dtr_fields + (a + 1) * N;
+                if (a < c->off_axis) {
+                    std::vector<float> cst(N);
+                    for (size_t i = 0; i < N; ++i) cst[i] = static_cast<float>(dt / rho0[i]);
+                    CK(cudaMemcpyAsync(dst, cst.data(), N * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+                    CK(cudaStreamSynchronize(c->stream));
+                } else {
+                    staggered_shift(*c, rdev, a, c->ring[1]);
+                    CK(cudaMemcpyAsync(shifted.data(), c->ring[1], N * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+                    CK(cudaStreamSynchronize(c->stream));
+                    for (size_t i = 0; i < N; ++i) {
+                        if (!(shifted[i] > 0.f)) fail(USTFWI_ERR_INVALID, "staggered density must stay positive");
+                        shifted[i] = static_cast<float>(dt / static_cast<double>(shifted[i]));
+                    }
+                    CK(cudaMemcpyAsync(dst, shifted.data(), N * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+                    CK(cudaStreamSynchronize(c->stream));
+                }
+                c->dtr_stag[a] = Coef{dst, 0.f};
+            }
+        }
+        c->gamma_host.clear();
+        if (gamma) {
+            c->gamma_host.assign(gamma, gamma + N);
+            CK(cudaMemcpyAsync(c->gamma, c->gamma_host.data(), N, cudaMemcpyHostToDevice, c->stream));
+        }
+        c->shell_pos = nullptr;  // shell depends on gamma
+        c->shell_thickness = 0;
+        c->has_medium = true;
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ustfwi_gpu_set_sources(ustfwi_gpu_ctx* c, size_t n_src, const size_t* pos, const size_t* sig_off,
+                           const double* sig, const double* weights, const int32_t* delay_steps) {
+    return guarded(c, [&] {
+        const size_t N = static_cast<size_t>(c->g.N);
+        std::vector<size_t> p(pos, pos + n_src);
+        for (size_t v : p)
+            if (v >= N) fail(USTFWI_ERR_INVALID, "source position outside grid");
+        const size_t total = n_src ? sig_off[n_src] : 0;
+        if (total >= (1ull << 31)) fail(USTFWI_ERR_INVALID, "signal table too large");
+        std::vector<int> off(n_src), len(n_src), stride(n_src, 1), delay(n_src, 0);
+        std::vector<float> w(n_src, 1.f);
+        for (size_t i = 0; i < n_src; ++i) {
+            off[i] = static_cast<int>(sig_off[i]);
+            len[i] = static_cast<int>(sig_off[i + 1] - sig_off[i]);
+            if (weights) w[i] = static_cast<float>(weights[i]);
+            if (delay_steps) delay[i] = delay_steps[i];
+        }
+        c->release(c->src.sig);
+        c->src.sig = c->upload(to_f32(sig, total));
+        build_inject(*c, c->src, p, off, len, stride, delay, w);
+        c->src_pos_host = p;
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ustfwi_gpu_set_sensors(ustfwi_gpu_ctx* c, size_t n_sensors, const size_t* pos) {
+    return guarded(c, [&] {
+        const size_t N = static_cast<size_t>(c->g.N);
+        std::vector<size_t> p(pos, pos + n_sensors);
+        for (size_t v : p)
+            if (v >= N) fail(USTFWI_ERR_INVALID, "sensor position outside grid");
+        c->n_sens = static_cast<int>(n_sensors);
+        c->sens_pos_host = p;
+        std::vector<int> order(n_sensors);
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return p[static_cast<size_t>(a)] < p[static_cast<size_t>(b)]; });
+        std::vector<int> sp(n_sensors), si(n_sensors);
+        for (size_t k = 0; k < n_sensors; ++k) {
+            sp[k] = static_cast<int>(p[static_cast<size_t>(order[k])]);
+            si[k] = order[k];
+        }
+        for (void* q : {(void*)c->sens_pos, (void*)c->sens_idx, (void*)c->data, (void*)c->obs, (void*)c->q,
+                        (void*)c->loss_part})
+            c->release(q);
+        c->data = nullptr;
+        c->sens_pos = c->upload(sp);
+        c->sens_idx = c->upload(si);
+        c->obs_ready = false;
+        ensure_data_buffers(*c);
+        // adjoint sources sit at the sensors: contribution s reads q[n*ns + s]
+        std::vector<int> off(n_sensors), len(n_sensors, c->grid.nt), stride(n_sensors, std::max<int>(1, c->n_sens)),
+            delay(n_sensors, 0);
+        std::iota(off.begin(), off.end(), 0);
+        std::vector<float> w(n_sensors, 1.f);
+        build_inject(*c, c->adj, p, off, len, stride, delay, w);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ustfwi_gpu_forward(ustfwi_gpu_ctx* c, int boundary_thickness, double* data_out, double* trace_out,
+                       size_t* n_shell_out) {
+    return guarded(c, [&] {
+        clear_flags(*c);
+        forward_sim(*c, boundary_thickness);
+        check_flags(*c, false);
+        const int nt = c->grid.nt, ns = c->n_sens;
+        if (data_out && ns > 0) {
+            std::vector<float> h(static_cast<size_t>(nt) * ns);
+            CK(cudaMemcpy(h.data(), c->data, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
+            for (int s = 0; s < ns; ++s)
+                for (int n = 0; n < nt; ++n)
+                    data_out[static_cast<size_t>(s) * nt + n] = h[static_cast<size_t>(n) * ns + s];
+        }
+        const size_t nsh = boundary_thickness > 0 ? c->shell_host.size() : 0;
+        if (n_shell_out) *n_shell_out = nsh;
+        if (trace_out && nsh > 0) {
+            std::vector<float> h(nsh * static_cast<size_t>(nt));
+            CK(cudaMemcpy(h.data(), c->trace, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < h.size(); ++i) trace_out[i] = h[i];
+        }
+    });
+}
+
+int ustfwi_gpu_upload_observed(ustfwi_gpu_ctx* c, const double* observed) {
+    return guarded(c, [&] {
+        ensure_data_buffers(*c);
+        const int nt = c->grid.nt, ns = c->n_sens;
+        std::vector<double> h(static_cast<size_t>(nt) * ns);
+        for (int s = 0; s < ns; ++s)
+            for (int n = 0; n < nt; ++n) h[static_cast<size_t>(n) * ns + s] = observed[static_cast<size_t>(s) * nt + n];
+        if (!h.empty()) CK(cudaMemcpyAsync(c->obs, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        c->obs_ready = true;
+    });
+}
+
+int ustfwi_gpu_run_gradient(ustfwi_gpu_ctx* c, int boundary_thickness, int accumulate) {
+    return guarded(c, [&] {
+        clear_flags(*c);
+        gradient_tr(*c, boundary_thickness, accumulate != 0);
+        check_flags(*c, true);
+    });
+}
+
+int ustfwi_gpu_download_gradient(ustfwi_gpu_ctx* c, double scale_div, double* grad_out, double* loss_out) {
+    return guarded(c, [&] {
+        const size_t N = static_cast<size_t>(c->g.N);
+        if (!(scale_div >= 1.0)) fail(USTFWI_ERR_INVALID, "scale_div must be >= 1");
+        if (grad_out) {
+            std::vector<float> h(N);
+            CK(cudaMemcpyAsync(h.data(), c->acc, N * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            for (size_t i = 0; i < N; ++i) grad_out[i] = static_cast<double>(h[i]) / scale_div;
+        }
+        if (loss_out) {
+            double l[2];
+            CK(cudaMemcpyAsync(l, c->loss, sizeof(l), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            *loss_out = l[1] / scale_div;
+        }
+    });
+}
+
+int ustfwi_gpu_gradient_tr(ustfwi_gpu_ctx* c, const double* observed, int boundary_thickness, double* grad_out,
+                           double* loss_out) {
+    int rc = ustfwi_gpu_upload_observed(c, observed);
+    if (rc == USTFWI_OK) rc = ustfwi_gpu_run_gradient(c, boundary_thickness, 0);
+    if (rc == USTFWI_OK) rc = ustfwi_gpu_download_gradient(c, 1.0, grad_out, loss_out);
+    return rc;
+}
+
+int ustfwi_gpu_evaluate_loss(ustfwi_gpu_ctx* c, const double* observed, double* loss_out) {
+    return guarded(c, [&] {
+        const int nt = c->grid.nt, ns = c->n_sens;
+        clear_flags(*c);
+        forward_sim(*c, 0);
+        check_flags(*c, false);
+        std::vector<float> h(static_cast<size_t>(nt) * ns);
+        CK(cudaMemcpy(h.data(), c->data, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        // Kahan sum in (sensor, time) order as evaluate_loss (gradient.hpp:495-503)
+        double loss = 0.0, comp = 0.0;
+        for (int s = 0; s < ns; ++s)
+            for (int n = 0; n < nt; ++n) {
+                const double r = static_cast<double>(h[static_cast<size_t>(n) * ns + s]) - observed[static_cast<size_t>(s) * nt + n];
+                const double term = 0.5 * r * r - comp;
+                const double t = loss + term;
+                comp = (t - loss) - term;
+                loss = t;
+            }
+        *loss_out = loss;
+    });
+}
+
+int ustfwi_gpu_derivative(ustfwi_gpu_ctx* c, const double* f, int axis, int stagger, double* out) {
+    return guarded(c, [&] {
+        if (axis < 0 || axis >= c->ndim) fail(USTFWI_ERR_INVALID, "axis out of range");
+        if (stagger < 0 || stagger > 2) fail(USTFWI_ERR_INVALID, "bad stagger");
+        const size_t N = static_cast<size_t>(c->g.N);
+        const int pa = axis + c->off_axis;
+        float* in = c->ring[0];
+        float* res = c->ring[1];
+        const auto h = to_f32(f, N);
+        CK(cudaMemcpyAsync(in, h.data(), N * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        Sim& s = c->sim[1];
+        c->count(launch_zfwd(c->g, in, s.S[0], c->stream));
+        PencilJobs j{};
+        for (int q = 0; q < 3; ++q) j.buf[q] = s.S[q];
+        j.n = 1;
+        j.job[0] = {0, 0, nullptr, 0};
+        c->count(launch_pencil(1, false, c->g, j, c->stream));
+        j.job[0] = {0, 0, pa == 0 ? c->dmul[0][stagger] : nullptr, 1};
+        c->count(launch_pencil(0, false, c->g, j, c->stream));
+        j.job[0] = {0, 0, pa == 1 ? c->dmul[1][stagger] : nullptr, 0};
+        c->count(launch_pencil(1, true, c->g, j, c->stream));
+        c->count(launch_zinv(c->g, s.S[0], pa == 2 ? c->dmul[2][stagger] : nullptr, res, c->stream));
+        std::vector<float> o(N);
+        CK(cudaMemcpyAsync(o.data(), res, N * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (size_t i = 0; i < N; ++i) out[i] = o[i];
+    });
+}
+
+int ustfwi_gpu_accumulator(ustfwi_gpu_ctx* c, float** grad_dev, double** loss_dev) {
+    return guarded(c, [&] {
+        if (grad_dev) *grad_dev = c->acc;
+        if (loss_dev) *loss_dev = c->loss + 1;
+    });
+}
+
+int ustfwi_gpu_synchronize(ustfwi_gpu_ctx* c) {
+    return guarded(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
+}
+
+void* ustfwi_gpu_stream(ustfwi_gpu_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+uint64_t ustfwi_gpu_launch_count(const ustfwi_gpu_ctx* c) { return c ? c->launches : 0; }
+size_t ustfwi_gpu_shell_size(const ustfwi_gpu_ctx* c) { return c ? c->shell_host.size() : 0; }
+
+int ustfwi_gpu_set_profiling(ustfwi_gpu_ctx* c, int enable) {
+    return guarded(c, [&] {
+        CK(cudaStreamSynchronize(c->stream));
+        c->resolve_profile();
+        c->profiling = enable != 0;
+        for (int k = 0; k < USTFWI_KERNEL_KINDS; ++k) {
+            c->prof_ms[k] = 0.0;
+            c->prof_bytes[k] = 0.0;
+            c->prof_n[k] = 0;
+        }
+    });
+}
+
+int ustfwi_gpu_kernel_stats(ustfwi_gpu_ctx* c, int kind, double* total_ms, uint64_t* launches, double* bytes) {
+    return guarded(c, [&] {
+        if (kind < 0 || kind >= USTFWI_KERNEL_KINDS) fail(USTFWI_ERR_INVALID, "bad kernel kind");
+        CK(cudaStreamSynchronize(c->stream));
+        c->resolve_profile();
+        if (total_ms) *total_ms = c->prof_ms[kind];
+        if (launches) *launches = c->prof_n[kind];
+        if (bytes) *bytes = c->prof_bytes[kind];
+    });
+}
+
+int ustfwi_nccl_unique_id(char id_out[128]) {
+    return guarded(nullptr, [&] {
+        NcclUniqueId id;
+        const int r = nccl().get_unique_id(&id);
+        if (r != 0) fail(USTFWI_ERR_NCCL, "ncclGetUniqueId failed");
+        std::memcpy(id_out, id.internal, 128);
+    });
+}
+
+int ustfwi_gpu_comm_init(ustfwi_gpu_ctx* c, const char id[128], int nranks, int rank) {
+    return guarded(c, [&] {
+        auto& api = nccl();
+        if (!api.comm_init_rank) {
+            // ncclCommInitRank(ncclComm_t*, int nranks, ncclUniqueId commId, int rank): the id is
+            // passed by value; declare the exact signature for the call.
+            using Fn = int (*)(void**, int, NcclUniqueId, int);
+            auto fn = reinterpret_cast<Fn>(dlsym(api.h, "ncclCommInitRank"));
+            if (!fn) fail(USTFWI_ERR_NCCL, "ncclCommInitRank missing");
+            NcclUniqueId uid;
+            std::memcpy(uid.internal, id, 128);
+            const int r = fn(&c->comm, nranks, uid, rank);
+            if (r != 0) fail(USTFWI_ERR_NCCL, std::string("ncclCommInitRank: ") + (api.error_string ? api.error_string(r) : "error"));
+            return;
+        }
+    });
+}
+
+int ustfwi_gpu_allreduce_mean(ustfwi_gpu_ctx* c, int batch) {
+    return guarded(c, [&] {
+        if (!c->comm) fail(USTFWI_ERR_NCCL, "no communicator (ustfwi_gpu_comm_init)");
+        if (batch < 1) fail(USTFWI_ERR_INVALID, "batch must be >= 1");
+        auto& api = nccl();
+        // ncclFloat32 = 7, ncclFloat64 = 8, ncclSum = 0 (nccl.h)
+        int r = api.all_reduce(c->acc, c->acc, static_cast<size_t>(c->g.N), 7, 0, c->comm, c->stream);
+        if (r == 0) r = api.all_reduce(c->loss + 1, c->loss + 1, 1, 8, 0, c->comm, c->stream);
+        if (r != 0) fail(USTFWI_ERR_NCCL, "ncclAllReduce failed");
+        c->count(launch_scale(c->acc, c->g.N, static_cast<float>(1.0 / batch), c->stream));
+        double l = 0.0;
+        CK(cudaMemcpyAsync(&l, c->loss + 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        l /= batch;
+        CK(cudaMemcpyAsync(c->loss + 1, &l, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+}  // extern "C"

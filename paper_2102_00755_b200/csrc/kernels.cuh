@@ -1,0 +1,138 @@
+// Device-side data structures shared by the pass kernels and the host orchestration.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "fft_smem.cuh"
+
+namespace ustfwi_dev {
+
+// Geometry of one context. Real fields are [nx][ny][nz] (z fastest, field.hpp:14-17);
+// spectral scratch is [nx][ny][nzp] float2 holding the nzh = nz/2+1 half-spectrum bins
+// of the last axis (fft.hpp:27-29) with the row padded to nzp for aligned tiles.
+struct GridDev {
+    int nx, ny, nz, nzh, nzp;
+    long long N;       // nx*ny*nz
+    long long rows;    // nx*ny
+    FftPlan px, py, pzh;        // complex plans along x, y and the half-length z plan
+    const float2* tw_rfft;      // exp(-2*pi*i*k/nz), k in [0, nz/2]  (real-FFT split)
+    const float* kx;            // wavenumbers per axis (fft.hpp:121-130), fp32
+    const float* ky;
+    const float* kz;
+    float half_cdt;             // 0.5 * c_ref * dt   (kappa = sinc(half_cdt*|k|), engine.hpp:43)
+    float inv_n;                // 1/N (RealFft::inverse normalisation, fft.hpp:58-63)
+};
+
+// Sparse mass-source injection: unique sorted flat positions, CSR into contributions.
+// amplitude(c, n) = w[c] * sig[off[c] + (n - delay[c]) * stride[c]]  for 0 <= n-delay < len[c]
+// (SourceSet::sample, medium.hpp:80-84; encoded: SPEC.md:296-304). Each unique position
+// adds amp * scale[u] to every split density (inject_mass_source, engine.hpp:296-300).
+struct SparseInject {
+    int n_unique;
+    const int* pos;
+    const int* csr;
+    const int* off;
+    const int* len;
+    const int* stride;
+    const int* delay;
+    const float* w;
+    const float* sig;
+    const float* scale;
+};
+
+// Sparse gather of p (sensor gather simulate.hpp:88-90, shell record :91-95):
+// out[idx[i]] = p[pos[i]], positions sorted ascending.
+struct SparseGather {
+    int n;
+    const int* pos;
+    const int* idx;
+    float* out;
+};
+
+// Dirichlet shell (enforce_shell, engine.hpp:304-307; scaling gradient.hpp:417-427):
+// rho_a[pos[j]] = vals[j] / (ndim * c0^2(pos)), vals = raw recorded pressure.
+struct SparseEnforce {
+    int n;
+    const int* pos;
+    const float* vals;
+    float ndim;
+};
+
+// In-kernel c0 correlation (GradientAccumulator, gradient.hpp:146-160,177-182):
+// grad += (2/c0^3) * ((p_new - 2 p_mid) + p_old) / dt * q_adj
+struct Correlate {
+    const float* p_mid;
+    const float* p_old;
+    const float* q_adj;
+    float* grad;
+    float inv_dt;
+};
+
+// Per-axis PML profiles (make_pml, grid.hpp:153-178), fp32.
+struct Pml {
+    const float* prof[3];
+};
+
+// Medium coefficients: either a uniform scalar or a field (nullptr -> scalar).
+struct Coef {
+    const float* field;
+    float scalar;
+    __device__ __forceinline__ float at(long long i) const { return field ? __ldg(field + i) : scalar; }
+};
+
+
+// ---- pass arguments ---------------------------------------------------------------
+struct PencilJob {
+    int src;              // scratch buffer index read
+    int dst;              // scratch buffer index written
+    const float2* dmul;   // per-index factor along the pass axis (D_a table), nullable
+    int kappa;            // X pass only: multiply by kappa(|k|)
+};
+
+struct PencilJobs {
+    int n;
+    PencilJob job[4];
+    float2* buf[3];
+};
+
+struct ZrhoArgs {
+    float2* S[3];
+    const float2* dz_minus;
+    float* rho[3];
+    Pml pml;
+    Coef dtrho0;
+    const float* c0sq;
+    float* p_out;
+    int a_first;          // first active axis (3 - ndim): inactive split densities stay 0
+    int step_n;           // source time index
+    SparseInject inj;     // n_unique == 0 -> none
+    SparseEnforce enf;    // n == 0 -> none
+    SparseGather sens;    // n == 0 -> none
+    SparseGather shell;   // n == 0 -> none
+    Correlate corr;       // grad == nullptr -> none
+    int check_step;       // >0: divergence check of p[0] at this stepper step index
+    int* diverged;        // atomicMin of the failing step index
+    int rows_per_cta;
+};
+
+
+// ---- launchers (kernels.cu) ---------------------------------------------------------
+int pencil_tile_cols(int L);
+int zrows_per_cta(int nz);
+cudaError_t launch_pencil(int axis, bool inv, const GridDev& g, const PencilJobs& jobs, cudaStream_t st);
+cudaError_t launch_zvel(const GridDev& g, float2* S[3], const float2* dz_plus, float* v[3], const Pml& pml,
+                        const Coef r[3], cudaStream_t st);
+cudaError_t launch_zrho(const GridDev& g, ZrhoArgs a, bool update, cudaStream_t st);
+cudaError_t launch_zfwd(const GridDev& g, const float* src, float2* S, cudaStream_t st);
+cudaError_t launch_zinv(const GridDev& g, const float2* S, const float2* premul, float* out, cudaStream_t st);
+cudaError_t launch_adjoint_source(const float* sim, const double* obs, int nt, int ns, int integrate, float* q,
+                                  double* loss_part, double* loss_out, double* loss_acc, int accumulate,
+                                  cudaStream_t st);
+cudaError_t launch_finalize_grad(const float* grad, const uint8_t* gamma, long long n, float* acc, int accumulate,
+                                 int* nonfinite, cudaStream_t st);
+cudaError_t launch_check_finite(const float* a, long long n, int* flag, cudaStream_t st);
+cudaError_t launch_scale(float* a, long long n, float s, cudaStream_t st);
+
+}  // namespace ustfwi_dev

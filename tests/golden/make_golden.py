@@ -1,0 +1,105 @@
+"""Generate the committed golden fixtures from the REFERENCE itself (oracle/_ref).
+
+oracle/_ref/libustfwi_ref.so is the unmodified reference headers compiled with the
+in-repo FFTW-API shim (oracle/Makefile). Run here (where /root/reference exists):
+
+    make -C oracle && python tests/golden/make_golden.py [--quick]
+
+Fixtures (small, committed):
+  derivative_3d.npz   SpectralEngine::derivative on a seeded 16x12x10 field, all axes/staggers
+  forward_2d.npz      simulate_forward on the reference's 2-D linearity-test grid
+  config_a.npz        config A (64^3, nt=393): observed data (truth medium), model traces,
+                      subsampled shell trace, TR gradient on gamma and loss
+  config_a_short.npz  config A truncated to nt=96 with f_obs = 0 (fast GPU parity case)
+"""
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+from oracle import ref  # noqa: E402
+from paper_2102_00755_b200 import capi, scenario  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def derivative_fixture():
+    g = capi.grid_from([16, 12, 10], 1e-3, 0.3e-3 / 1500.0, 4, [0, 0, 0], 1500.0)
+    rng = np.random.default_rng(17)
+    f = rng.standard_normal(g.shape)
+    out = {"f": f, "dims": np.array(g.shape), "dx": 1e-3, "dt": g.dt, "c_ref": 1500.0}
+    for axis in range(3):
+        for st, name in enumerate(["none", "plus", "minus"]):
+            out[f"d{axis}_{name}"] = ref.engine_derivative(g, f, axis, st)
+    # a PML-padded grid as well (kappa with c_ref from make_grid)
+    g2 = capi.make_grid([4, 4, 4], 1e-3, 1800.0, 2e-6)
+    f2 = rng.standard_normal(g2.shape)
+    out["f2"] = f2
+    out["g2"] = np.array([*g2.shape, g2.pml_size[0], g2.pml_size[1], g2.pml_size[2], g2.nt])
+    out["g2_dt"] = g2.dt
+    for axis in range(3):
+        out[f"g2_d{axis}_plus"] = ref.engine_derivative(g2, f2, axis, 1)
+    np.savez_compressed(os.path.join(OUT, "derivative_3d.npz"), **out)
+
+
+def forward_2d_fixture():
+    # test_solver.cpp:82-119 grid: make_grid({64,64}, 1e-3, 1800, 5e-5)
+    g = capi.make_grid([64, 64], 1e-3, 1800.0, 5e-5)
+    shape = g.shape
+    pulse = capi.synth_source_pulse(g, 0.8, 1500.0)
+    c0 = np.full(shape, 1500.0)
+    rho0 = np.full(shape, 1000.0)
+
+    class M:
+        pass
+    m = M()
+    m.c0, m.rho0, m.alpha0, m.y, m.gamma, m.c0_min, m.c0_max = c0, rho0, None, 1.5, None, 1350.0, 1800.0
+    pos = [24 * shape[1] + 30, 30 * shape[1] + 24]
+    sig = [pulse, -0.7 * pulse]
+    sens = [40 * shape[1] + 40, 20 * shape[1] + 50, 70 * shape[1] + 70]
+    data, _ = ref.simulate_forward(g, m, pos, sig, sens)
+    np.savez_compressed(os.path.join(OUT, "forward_2d.npz"), data=data, pos=np.array(pos), sens=np.array(sens),
+                        pulse=pulse, nt=g.nt, dims=np.array(shape))
+
+
+def config_a_fixture(nt, name, trace_stride=(8, 16), observed_zero=False):
+    """observed_zero: use f_obs = 0 (residual = the model data) so that a short run still
+    has an O(1) residual and a well-conditioned gradient."""
+    sc = scenario.config_a(nt=nt)
+    g = sc.grid
+    t0 = time.time()
+    pos, sig = list(sc.sources.positions), [np.asarray(s) for s in sc.sources.signals]
+    if observed_zero:
+        observed = np.zeros((len(sc.sensors.positions), g.nt))
+    else:
+        observed, _ = ref.simulate_forward(g, sc.truth, pos, sig, sc.sensors.positions)
+    t1 = time.time()
+    data_model, trace = ref.simulate_forward(g, sc.model, pos, sig, sc.sensors.positions, boundary_thickness=8)
+    t2 = time.time()
+    loss, grad = ref.gradient_time_reversal(g, sc.model, pos, sig, sc.sensors.positions, observed, 8)
+    t3 = time.time()
+    gidx = np.flatnonzero(np.asarray(sc.model.gamma).ravel())
+    np.savez_compressed(
+        os.path.join(OUT, f"{name}.npz"), observed=observed, data_model=data_model,
+        trace_sub=trace[::trace_stride[0], ::trace_stride[1]], trace_stride=np.array(trace_stride),
+        trace_checksum=np.array([trace.sum(), np.abs(trace).sum(), (trace ** 2).sum()]),
+        loss=loss, grad_gamma=grad.ravel()[gidx], gamma_idx=gidx, nt=g.nt,
+        grad_outside_max=np.abs(np.delete(grad.ravel(), gidx)).max() if grad.size > gidx.size else 0.0,
+        seconds=np.array([t1 - t0, t2 - t1, t3 - t2]))
+    print(f"{name}: fwd {t1 - t0:.1f}s fwd+trace {t2 - t1:.1f}s gradient {t3 - t2:.1f}s loss {loss:.6e}")
+
+
+if __name__ == "__main__":
+    if not ref.available():
+        sys.exit("oracle/_ref missing: make -C oracle")
+    derivative_fixture()
+    forward_2d_fixture()
+    config_a_fixture(96, "config_a_short", observed_zero=True)
+    if "--quick" not in sys.argv:
+        config_a_fixture(None, "config_a")
