@@ -91,8 +91,9 @@ std::vector<double> wavenumbers(int n, double dx) {
     std::vector<double> k(static_cast<size_t>(n));
     const double dk = 2.0 * M_PI / (static_cast<double>(n) * dx);
     for (int m = 0; m < n; ++m) {
-        // bins 0..n/2-1 positive, n/2..n-1 negative (the Nyquist bin is -n/2)
-        const int signed_m = (m < n / 2) ? m : m - n;
+        // bins 0..n/2-1 positive, n/2..n-1 negative; the Nyquist bin n/2 is -n/2, which
+        // also makes the single bin of a length-1 (padded singleton) axis zero
+        const int signed_m = (m < n / 2) ? m : (m == n / 2 ? -(n / 2) : m - n);
         k[static_cast<size_t>(m)] = dk * signed_m;
     }
     return k;

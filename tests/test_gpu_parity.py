@@ -259,3 +259,22 @@ def test_heterogeneous_density_staggering():
     want, _ = orc.simulate_forward(orc.Grid.of(g), c0, rho0, src, [pulse], sens)
     res = simulate_forward(Medium(c0=c0, rho0=rho0), SourceSet(src, [pulse]), SensorArray(sens), g)
     assert rel(res.data, want) < TRACE_TOL
+
+
+@pytest.mark.parametrize("dims", [
+    (4, 6, 8), (10, 14, 18), (16, 96, 10), (12, 12, 96), (48, 12, 10), (6, 480, 6), (480, 4, 4),
+    (4, 4, 512), (14, 6, 14), (22, 4, 4), (4, 26, 6), (8, 8, 144), (144, 6, 8), (64, 64), (96, 96), (12, 256),
+    (256,), (90,),
+])
+def test_derivative_fft_sizes(dims):
+    """Every radix path of the device FFT (16/8/4/2/5/3/7 and the generic odd stage) on all
+    three pass kinds, 1-D/2-D/3-D, against the fp64 numpy restatement."""
+    from oracle import ustfwi_oracle as orc
+    g = capi.grid_from(list(dims), 1e-3, 0.3e-3 / 1800.0, 4, [0] * len(dims), 1800.0)
+    f = np.random.default_rng(sum(dims)).standard_normal(dims)
+    og = orc.Grid.of(g)
+    oe = orc.SpectralEngine(og)
+    with GpuEngine(g) as eng:
+        for axis in range(len(dims)):
+            for st in ("none", "plus", "minus"):
+                assert rel(eng.derivative(f, axis, st), oe.derivative(f, axis, st)) < 2e-5, (axis, st)
