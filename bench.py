@@ -211,7 +211,7 @@ def b200_arm(a):
         torch.cuda.set_device(local)
         dist.init_process_group("gloo")
     dev = local
-    sc = scenario.CONFIGS[a.config]()
+    sc = scenario.CONFIGS[a.config]() if a.nt is None else scenario.CONFIGS[a.config](nt=a.nt)
     g = sc.grid
     eng = E.GpuEngine(g, device=dev)
     if world > 1:
@@ -364,6 +364,7 @@ def main():
     p.add_argument("--cpu-baseline", type=int, default=1)
     p.add_argument("--cpu-sample-config", default="B")
     p.add_argument("--cpu-sample-steps", type=int, default=2)
+    p.add_argument("--nt", type=int, default=None, help="override nt (development only; not a valid bench number)")
     a = p.parse_args()
     if a.impl == "reference":
         return reference_arm(a)

@@ -24,15 +24,15 @@ struct FftPlan {
     const float2* tw;            // tw[k] = exp(-2*pi*i*k/L), k in [0, L)
 };
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+__host__ __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
-__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__host__ __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 // multiply by sign*i  (sign = -1 forward, +1 inverse)
 template <bool INV>
-__device__ __forceinline__ float2 mul_si(float2 a) {
+__host__ __device__ __forceinline__ float2 mul_si(float2 a) {
     return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
 }
 
@@ -43,7 +43,7 @@ struct Dft;
 
 template <bool INV>
 struct Dft<2, INV> {
-    __device__ __forceinline__ static void run(float2* v) {
+    __host__ __device__ __forceinline__ static void run(float2* v) {
         const float2 a = v[0], b = v[1];
         v[0] = cadd(a, b);
         v[1] = csub(a, b);
@@ -52,7 +52,7 @@ struct Dft<2, INV> {
 
 template <bool INV>
 struct Dft<3, INV> {
-    __device__ __forceinline__ static void run(float2* v) {
+    __host__ __device__ __forceinline__ static void run(float2* v) {
         const float h = 0.86602540378443864676f;  // sqrt(3)/2
         const float2 s = cadd(v[1], v[2]);
         const float2 d = csub(v[1], v[2]);
@@ -66,7 +66,7 @@ struct Dft<3, INV> {
 
 template <bool INV>
 struct Dft<4, INV> {
-    __device__ __forceinline__ static void run(float2* v) {
+    __host__ __device__ __forceinline__ static void run(float2* v) {
         const float2 a = cadd(v[0], v[2]), b = csub(v[0], v[2]);
         const float2 c = cadd(v[1], v[3]), d = mul_si<INV>(csub(v[1], v[3]));
         v[0] = cadd(a, c);
@@ -78,7 +78,7 @@ struct Dft<4, INV> {
 
 template <bool INV>
 struct Dft<5, INV> {
-    __device__ __forceinline__ static void run(float2* v) {
+    __host__ __device__ __forceinline__ static void run(float2* v) {
         const float c1 = 0.30901699437494742410f, c2 = -0.80901699437494742410f;
         const float s1 = 0.95105651629515357212f, s2 = 0.58778525229247312917f;
         const float2 p1 = cadd(v[1], v[4]), m1 = csub(v[1], v[4]);
@@ -98,7 +98,7 @@ struct Dft<5, INV> {
 
 template <bool INV>
 struct Dft<7, INV> {
-    __device__ __forceinline__ static void run(float2* v) {
+    __host__ __device__ __forceinline__ static void run(float2* v) {
         const float c[3] = {0.62348980185873353053f, -0.22252093395631440429f,
                             -0.90096886790241912624f};
         const float s[3] = {0.78183148246802980871f, 0.97492791218182360702f,
@@ -133,7 +133,7 @@ struct Dft<7, INV> {
 
 template <bool INV>
 struct Dft<8, INV> {
-    __device__ __forceinline__ static void run(float2* v) {
+    __host__ __device__ __forceinline__ static void run(float2* v) {
         const float r = 0.70710678118654752440f;
         float2 a[4], b[4];
 #pragma unroll
@@ -159,7 +159,7 @@ struct Dft<8, INV> {
 
 template <bool INV>
 struct Dft<16, INV> {
-    __device__ __forceinline__ static void run(float2* v) {
+    __host__ __device__ __forceinline__ static void run(float2* v) {
         // 16 = 4 x 4: column DFTs, twiddle w16^(n1*k2), row DFTs
         float2 t[4][4];
 #pragma unroll

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -456,8 +457,17 @@ static cudaError_t launch_pencil_t(const GridDev& g, const PencilJobs& jobs, cud
 
 int pencil_tile_cols(int L) { return L <= 768 ? 8 : (L <= 1536 ? 4 : 2); }
 
+bool use_generic_kernels() {
+    static const bool generic = [] {
+        const char* e = getenv("USTFWI_GENERIC");
+        return e && e[0] == '1';
+    }();
+    return generic;
+}
+
 cudaError_t launch_pencil(int axis, bool inv, const GridDev& g, const PencilJobs& jobs, cudaStream_t st) {
     const int L = axis == 0 ? g.px.L : g.py.L;
+    if (!use_generic_kernels() && fast_pencil_supported(L)) return launch_pencil_fast(axis, inv, g, jobs, st);
     const int tb = pencil_tile_cols(L);
     if (axis == 0) {
         if (tb == 8) return launch_pencil_t<0, 8, false>(g, jobs, st);
@@ -485,6 +495,7 @@ static size_t zsmem_bytes(int nz, int R) { return (size_t)5 * R * nz * sizeof(fl
 
 cudaError_t launch_zvel(const GridDev& g, float2* S[3], const float2* dz_plus, float* v[3], const Pml& pml,
                         const Coef r[3], cudaStream_t st) {
+    if (!use_generic_kernels() && fast_rows_supported(g.nz)) return launch_zvel_fast(g, S, dz_plus, v, pml, r, st);
     const int R = zrows_per_cta(g.nz);
     static bool configured = false;
     if (!configured) {
@@ -498,6 +509,7 @@ cudaError_t launch_zvel(const GridDev& g, float2* S[3], const float2* dz_plus, f
 }
 
 cudaError_t launch_zrho(const GridDev& g, ZrhoArgs a, bool update, cudaStream_t st) {
+    if (update && !use_generic_kernels() && fast_rows_supported(g.nz)) return launch_zrho_fast(g, a, st);
     const int R = zrows_per_cta(g.nz);
     a.rows_per_cta = R;
     static bool configured = false;

@@ -135,4 +135,13 @@ cudaError_t launch_finalize_grad(const float* grad, const uint8_t* gamma, long l
 cudaError_t launch_check_finite(const float* a, long long n, int* flag, cudaStream_t st);
 cudaError_t launch_scale(float* a, long long n, float s, cudaStream_t st);
 
+// register-resident fast paths (passes.cu) for the compiled transform lengths
+bool fast_pencil_supported(int L);
+bool fast_rows_supported(int nz);
+cudaError_t launch_pencil_fast(int axis, bool inv, const GridDev& g, const PencilJobs& jobs, cudaStream_t st);
+cudaError_t launch_zvel_fast(const GridDev& g, float2* S[3], const float2* dz_plus, float* v[3], const Pml& pml,
+                             const Coef r[3], cudaStream_t st);
+cudaError_t launch_zrho_fast(const GridDev& g, const ZrhoArgs& a, cudaStream_t st);
+bool use_generic_kernels();
+
 }  // namespace ustfwi_dev

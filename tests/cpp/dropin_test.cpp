@@ -25,7 +25,7 @@ int main() {
     EXPECT(choose_pml_size({44}) == Dims{10});
     EXPECT(choose_pml_size({100}) == Dims{14});
     Grid g = make_grid({28, 28, 28}, 1e-3, 1800.0, 3e-5);
-    EXPECT(g.dims == (Dims{48, 48, 48}));
+    EXPECT(g.dims == (Dims{64, 64, 64}));  // 28 + 2*18: the 2-smooth padding
     Medium m = make_homogeneous_medium(g);
     auto pulse = synth_source_pulse(g, 0.8, 1500.0);
     SpectralEngine eng(g);
@@ -60,7 +60,7 @@ int main() {
     EXPECT(den > 0 && std::sqrt(num / den) < 1e-5);
 
     // TR gradient (gradient.hpp:478-488): zero residual -> zero gradient; gradient zero outside gamma
-    m.gamma = ball_mask(g.dims, {24, 24, 24}, 9.0);
+    m.gamma = ball_mask(g.dims, {32, 32, 32}, 9.0);
     SensorData obs = r1.data;
     auto gr = gradient_time_reversal(m, s1, sensors, obs, g, 4, GradientParam::c0, &eng);
     EXPECT(gr.loss == 0.0 && max_abs(gr.grad) == 0.0);
