@@ -356,8 +356,12 @@ void run_step(Ctx& c, Sim& s, const StepIO& io) {
     a.corr = io.corr;
     a.check_step = io.check_step;
     a.diverged = c.flags;
-    const double zb = 4 * SB + 8 * FB + (c.dtrho0.field ? FB : 0.0) + (io.corr.grad ? 5 * FB : 0.0);
+    // the fast path splits the step into the per-axis density update and the pressure
+    // kernel, which re-reads the three split densities (+3F)
+    const bool split = !use_generic_kernels() && fast_rows_supported(g.nz);
+    const double zb = 4 * SB + (split ? 11 : 8) * FB + (c.dtrho0.field ? FB : 0.0) + (io.corr.grad ? 5 * FB : 0.0);
     c.launch(KIND_ZRHO, zb, [&] { return launch_zrho(g, a, true, c.stream); });
+    if (split) ++c.launches;
 }
 
 // Build the device InjectSet for `n` contributions at flat positions pos[i].

@@ -17,6 +17,8 @@
 // sparse sources and shell, gathers and the c0 correlation in the same kernel.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "async_copy.cuh"
 #include "fft_reg.cuh"
 #include "kernels.cuh"
@@ -27,152 +29,233 @@ __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.
 
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
+// kappa = sinc(h|k|) = sin(sqrt(u))/sqrt(u), u = (h|k|)^2, h = c_ref*dt/2 (engine.hpp:43).
+// sinc(sqrt(u)) = sum_n (-u)^n / (2n+1)! is entire in u; with u <= 3 (the CFL bound
+// c*dt/dx <= 2/pi gives h|k| <= sqrt(3)) eleven Horner terms are exact to < 1e-9, so no
+// sin / sqrt / division is evaluated per spectral element.
 __device__ __forceinline__ float kappa_fast(float k2, float half_cdt) {
-    const float x = half_cdt * sqrtf(k2);
-    return (x < 1e-4f) ? 1.f - x * x * (1.f / 6.f) : sinf(x) / x;
+    const float u = half_cdt * half_cdt * k2;
+    float s = -1.f / 51090942171709440000.f;  // -1/21!
+    s = fmaf(s, u, 1.f / 121645100408832000.f);
+    s = fmaf(s, u, -1.f / 355687428096000.f);
+    s = fmaf(s, u, 1.f / 1307674368000.f);
+    s = fmaf(s, u, -1.f / 6227020800.f);
+    s = fmaf(s, u, 1.f / 39916800.f);
+    s = fmaf(s, u, -1.f / 362880.f);
+    s = fmaf(s, u, 1.f / 5040.f);
+    s = fmaf(s, u, -1.f / 120.f);
+    s = fmaf(s, u, 1.f / 6.f);
+    return fmaf(-s, u, 1.f);
 }
 
 // ======================================================================================
 // Pencil passes (x and y)
 // ======================================================================================
-template <int L, int N1, int TB>
+template <int L, int N1, int TB, bool DB>
 struct PencilCfg {
     static constexpr int N2 = L / N1;
     static constexpr int NT = TB * cmax(N1, N2);
     static constexpr int KP = N2 * TB + 8;  // float2 pitch of one k1 slab (+64 B against bank conflicts)
-    static constexpr size_t SMEM = (size_t(L) * TB + size_t(N1) * KP + L) * sizeof(float2);
+    // Good-Thomas split when gcd(N1, N2) == 1: no inter-level twiddles
+    static constexpr bool PFA = cx_gcd(N1, N2) == 1;
+    static constexpr int CR = PFA ? (N2 * cx_inv_mod(N2 % N1, N1)) % L : 0;  // = 1 mod N1, 0 mod N2
+    static constexpr int CM = PFA ? (N1 * cx_inv_mod(N1 % N2, N2)) % L : 0;  // = 0 mod N1, 1 mod N2
+    // tile buffer(s) (two with double-buffered prefetch) + transpose tile + twiddles
+    static constexpr size_t SMEM = ((DB ? 2 : 1) * size_t(L) * TB + size_t(N1) * KP + L) * sizeof(float2);
+    // row of input element (n1, n2) and of output element (k1, k2)
+    __device__ __forceinline__ static int in_row(int n1, int n2) {
+        if constexpr (PFA) {
+            const int t = N2 * n1 + N1 * n2;
+            return t >= L ? t - L : t;
+        } else {
+            return n2 + N2 * n1;
+        }
+    }
+    __device__ __forceinline__ static int out_row(int kbase, int k2) {  // kbase = out_base(k1)
+        if constexpr (PFA) {
+            const int t = kbase + (k2 * CM) % L;
+            return t >= L ? t - L : t;
+        } else {
+            return kbase + N1 * k2;
+        }
+    }
+    __device__ __forceinline__ static int out_base(int k1) { return PFA ? (k1 * CR) % L : k1; }
 };
 
-// AXIS 0: x pencils at fixed y = blockIdx.y (forward * multiplier * inverse per job).
-// AXIS 1: y pencils at fixed x = blockIdx.y, direction INV, optional premultiplier.
-template <int AXIS, bool INV, int L, int N1, int TB, int MINB>
-__global__ void __launch_bounds__(PencilCfg<L, N1, TB>::NT, MINB)
+// Persistent pencil pass. Work unit = (tile, source group): tile = TB consecutive spectral
+// columns of one line set (x pencils at fixed y for AXIS 0, y pencils at fixed x for AXIS 1);
+// a source group is a run of jobs reading the same scratch buffer. Each CTA walks its units
+// with the next unit's tile prefetched by cp.async into the other buffer while the
+// current one is transformed.
+//   AXIS 0: forward x FFT, kappa (and D_x of the job), inverse x FFT, one store per job.
+//   AXIS 1: y FFT in direction INV (inverse jobs may carry a D_y premultiplier).
+template <int AXIS, bool INV, int L, int N1, int TB, int MINB, bool DB>
+__global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
     pencil_fast_kernel(const __grid_constant__ GridDev g, const __grid_constant__ PencilJobs jobs) {
-    using C = PencilCfg<L, N1, TB>;
+    using C = PencilCfg<L, N1, TB, DB>;
     constexpr int N2 = C::N2, KP = C::KP, NT = C::NT;
     extern __shared__ float2 smem[];
-    float2* xs = smem;             // [L][TB] tile, natural order
-    float2* ys = xs + L * TB;      // transposed [N1][N2*TB (+pad)]
-    float2* tw = ys + N1 * KP;     // W_L^k
+    float2* xbuf0 = smem;                     // [L][TB] tiles, natural order
+    float2* xbuf1 = DB ? smem + L * TB : smem;
+    float2* ys = smem + (DB ? 2 : 1) * L * TB;  // transposed [N1][N2*TB (+pad)]
+    float2* tw = ys + N1 * KP;                // W_L^k
     const FftPlan& plan = AXIS == 0 ? g.px : g.py;
     for (int i = threadIdx.x; i < L; i += NT) tw[i] = plan.tw[i];
 
-    const int c0 = blockIdx.x * TB;
-    const int ncol = min(TB, g.nzh - c0);
+    // source groups of the job list
+    int gstart[5];
+    int ng = 0;
+    for (int jb = 0; jb < jobs.n; ++jb)
+        if (jb == 0 || jobs.job[jb].src != jobs.job[jb - 1].src) gstart[ng++] = jb;
+    gstart[ng] = jobs.n;
+
+    const int ntx = (g.nzh + TB - 1) / TB;
+    const int ntiles = ntx * (AXIS == 0 ? g.ny : g.nx);
+    const int nunits = ((ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * ng;
     const int pitch = (AXIS == 0) ? g.ny * g.nzp : g.nzp;
-    const long long base = (AXIS == 0) ? (long long)blockIdx.y * g.nzp + c0 : (long long)blockIdx.y * g.ny * g.nzp + c0;
     const int c = threadIdx.x % TB;
     const int ra = threadIdx.x / TB;  // n2 in phase A, k1 in phase B
     const bool inA = ra < N2, inB = ra < N1;
-    const bool colok = c < ncol;
 
-    // async tile load: 16-B granules (2 complex); columns past nzh are padding of the row
-    auto load_tile = [&](const float2* src) {
-        constexpr int CH = TB / 2;
-        const float2* s = src + base;
-        for (int i = threadIdx.x; i < L * CH; i += NT) {
-            const int row = i / CH, cc = 2 * (i % CH);
-            if (cc < ncol) cp_async16(xs + row * TB + cc, s + row * pitch + cc);
+    struct Unit {
+        int c0, ncol, line, grp;
+        long long base;
+    };
+    auto unit_of = [&](int u) {
+        Unit w;
+        const int tile = (int)blockIdx.x + (u / ng) * (int)gridDim.x;
+        w.grp = u % ng;
+        w.line = tile / ntx;
+        w.c0 = (tile % ntx) * TB;
+        w.ncol = min(TB, g.nzh - w.c0);
+        w.base = (AXIS == 0) ? (long long)w.line * g.nzp + w.c0 : (long long)w.line * g.ny * g.nzp + w.c0;
+        return w;
+    };
+    // async tile load: 16-B granules (2 complex); columns past nzh are row padding
+    auto prefetch = [&](int u, float2* xs) {
+        if (u < nunits) {
+            const Unit w = unit_of(u);
+            const float2* s = jobs.buf[jobs.job[gstart[w.grp]].src] + w.base;
+            constexpr int CH = TB / 2;
+            for (int i = threadIdx.x; i < L * CH; i += NT) {
+                const int row = i / CH, cc = 2 * (i % CH);
+                if (cc < w.ncol) cp_async16(xs + row * TB + cc, s + row * pitch + cc);
+            }
         }
         cp_async_commit();
-        cp_async_wait_all();
-        __syncthreads();
-    };
-    // forward transform of the tile in xs -> X[k1 + N1*k2] in phase-B registers
-    auto forward = [&](float2 (&X)[N2]) {
-        if (inA) {
-            float2 a[N1];
-#pragma unroll
-            for (int n1 = 0; n1 < N1; ++n1) a[n1] = xs[(ra + N2 * n1) * TB + c];
-            RDft<N1, false>::run(a);
-#pragma unroll
-            for (int k1 = 1; k1 < N1; ++k1) a[k1] = cmul(a[k1], tw[ra * k1]);
-#pragma unroll
-            for (int k1 = 0; k1 < N1; ++k1) ys[k1 * KP + ra * TB + c] = a[k1];
-        }
-        __syncthreads();
-        if (inB) {
-#pragma unroll
-            for (int n2 = 0; n2 < N2; ++n2) X[n2] = ys[ra * KP + n2 * TB + c];
-            RDft<N2, false>::run(X);
-        }
-    };
-    // inverse of b (phase-B registers, natural order) -> rows of dst
-    auto inverse_store = [&](float2 (&b)[N2], float2* dst) {
-        if (inB) {
-            RDft<N2, true>::run(b);
-#pragma unroll
-            for (int n2 = 1; n2 < N2; ++n2) b[n2] = cmul(b[n2], conjf2(tw[ra * n2]));
-        }
-        __syncthreads();
-        if (inB) {
-#pragma unroll
-            for (int n2 = 0; n2 < N2; ++n2) ys[ra * KP + n2 * TB + c] = b[n2];
-        }
-        __syncthreads();
-        if (inA) {
-            float2 a[N1];
-#pragma unroll
-            for (int k1 = 0; k1 < N1; ++k1) a[k1] = ys[k1 * KP + ra * TB + c];
-            RDft<N1, true>::run(a);
-            if (colok) {
-                float2* d = dst + base + c;
-#pragma unroll
-                for (int n1 = 0; n1 < N1; ++n1) d[(ra + N2 * n1) * pitch] = a[n1];
-            }
-        }
     };
 
-    int loaded = -1;
-    for (int jb = 0; jb < jobs.n; ++jb) {
-        const PencilJob J = jobs.job[jb];
-        if (J.src != loaded) {
-            load_tile(jobs.buf[J.src]);
-            loaded = J.src;
-            if (AXIS == 0) {
-                // forward, then keep kappa * X (natural order) in xs for the jobs of this source
-                float2 X[N2];
-                forward(X);
-                // (all jobs of one source share its kappa flag: true for every job list the
-                // engine builds; kappa-free jobs are the staggered-density setup shift)
-                if (inB) {
-                    const float ky = g.ky[blockIdx.y];
-                    const float kz = colok ? g.kz[c0 + c] : 0.f;
-#pragma unroll
-                    for (int k2 = 0; k2 < N2; ++k2) {
-                        const int k = ra + N1 * k2;
-                        const float kx = g.kx[k];
-                        xs[k * TB + c] =
-                            J.kappa ? cscale(X[k2], kappa_fast(kx * kx + ky * ky + kz * kz, g.half_cdt)) : X[k2];
-                    }
-                }
-                // each phase-B thread reads back only the entries it wrote: no barrier needed
-            }
+    if (DB) prefetch(0, xbuf0);
+    for (int u = 0; u < nunits; ++u) {
+        float2* xs = (u & 1) ? xbuf1 : xbuf0;
+        if constexpr (DB) {
+            prefetch(u + 1, (u & 1) ? xbuf0 : xbuf1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            prefetch(u, xs);
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         }
+        __syncthreads();
+        const Unit w = unit_of(u);
+        const bool colok = c < w.ncol;
+        const long long base = w.base;
+
+        // forward transform of xs -> X[k1 + N1*k2] in phase-B registers
+        auto forward = [&](float2 (&X)[N2]) {
+            if (inA) {
+                float2 a[N1];
+#pragma unroll
+                for (int n1 = 0; n1 < N1; ++n1) a[n1] = xs[C::in_row(n1, ra) * TB + c];
+                RDft<N1, false>::run(a);
+                if constexpr (!C::PFA) {
+#pragma unroll
+                    for (int k1 = 1; k1 < N1; ++k1) a[k1] = cmul(a[k1], tw[ra * k1]);
+                }
+#pragma unroll
+                for (int k1 = 0; k1 < N1; ++k1) ys[k1 * KP + ra * TB + c] = a[k1];
+            }
+            __syncthreads();
+            if (inB) {
+#pragma unroll
+                for (int n2 = 0; n2 < N2; ++n2) X[n2] = ys[ra * KP + n2 * TB + c];
+                RDft<N2, false>::run(X);
+            }
+        };
+        // inverse of b (phase-B registers, natural order) -> rows of dst
+        auto inverse_store = [&](float2 (&b)[N2], float2* dst) {
+            if (inB) {
+                RDft<N2, true>::run(b);
+                if constexpr (!C::PFA) {
+#pragma unroll
+                    for (int n2 = 1; n2 < N2; ++n2) b[n2] = cmul(b[n2], conjf2(tw[ra * n2]));
+                }
+            }
+            __syncthreads();
+            if (inB) {
+#pragma unroll
+                for (int n2 = 0; n2 < N2; ++n2) ys[ra * KP + n2 * TB + c] = b[n2];
+            }
+            __syncthreads();
+            if (inA) {
+                float2 a[N1];
+#pragma unroll
+                for (int k1 = 0; k1 < N1; ++k1) a[k1] = ys[k1 * KP + ra * TB + c];
+                RDft<N1, true>::run(a);
+                if (colok) {
+                    float2* d = dst + base + c;
+#pragma unroll
+                    for (int n1 = 0; n1 < N1; ++n1) d[C::in_row(n1, ra) * pitch] = a[n1];
+                }
+            }
+        };
+
+        const int kb = C::out_base(ra);
         if (AXIS == 1 && !INV) {
             float2 X[N2];
             forward(X);
             if (inB && colok) {
-                float2* d = jobs.buf[J.dst] + base + c;
+                float2* d = jobs.buf[jobs.job[gstart[w.grp]].dst] + base + c;
 #pragma unroll
-                for (int k2 = 0; k2 < N2; ++k2) d[(ra + N1 * k2) * pitch] = X[k2];
+                for (int k2 = 0; k2 < N2; ++k2) d[C::out_row(kb, k2) * pitch] = X[k2];
             }
-            __syncthreads();  // phase-B reads of ys done before the next tile's phase A
-            loaded = -1;
-            continue;
-        }
-        float2 b[N2];
-        if (inB) {
+        } else {
+            if (AXIS == 0) {
+                // forward, then keep kappa * X (natural order) in xs for the jobs of this group;
+                // all jobs of one source share its kappa flag (kappa-free jobs are only the
+                // staggered-density setup shift). Each phase-B thread later reads back only
+                // the entries it wrote, so no barrier is needed.
+                const bool kap = jobs.job[gstart[w.grp]].kappa != 0;
+                float2 X[N2];
+                forward(X);
+                if (inB) {
+                    const float ky = g.ky[w.line];
+                    const float kz = colok ? g.kz[w.c0 + c] : 0.f;
 #pragma unroll
-            for (int k2 = 0; k2 < N2; ++k2) {
-                const int k = ra + N1 * k2;
-                float2 v = xs[k * TB + c];
-                if (J.dmul) v = cmul(v, __ldg(J.dmul + k));
-                b[k2] = v;
+                    for (int k2 = 0; k2 < N2; ++k2) {
+                        const int k = C::out_row(kb, k2);
+                        const float kx = g.kx[k];
+                        xs[k * TB + c] = kap ? cscale(X[k2], kappa_fast(kx * kx + ky * ky + kz * kz, g.half_cdt)) : X[k2];
+                    }
+                }
+            }
+            for (int jb = gstart[w.grp]; jb < gstart[w.grp + 1]; ++jb) {
+                const PencilJob J = jobs.job[jb];
+                float2 b[N2];
+                if (inB) {
+#pragma unroll
+                    for (int k2 = 0; k2 < N2; ++k2) {
+                        const int k = C::out_row(kb, k2);
+                        float2 v = xs[k * TB + c];
+                        if (J.dmul) v = cmul(v, __ldg(J.dmul + k));
+                        b[k2] = v;
+                    }
+                }
+                inverse_store(b, jobs.buf[J.dst]);
             }
         }
-        inverse_store(b, jobs.buf[J.dst]);
+        __syncthreads();  // xs / ys free for the next prefetch into this buffer and the next unit
     }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 // ======================================================================================
@@ -183,6 +266,7 @@ struct RowCfg {
     static constexpr int N2 = M / N1;
     static constexpr int TPR = cmax(N1, N2);  // threads per row
     static constexpr int NT = RW * TPR;
+    static constexpr int NTG = (NT + 31) / 32 * 32;  // warp-aligned group size (named barriers)
     static constexpr int ZP = N2 + 1;         // transposed tile pitch (bank spread)
     static constexpr int ZT = N1 * ZP;        // float2 per row, transposed layout
     static constexpr int NZ = 2 * M;
@@ -285,33 +369,37 @@ struct Stager {
     }
 };
 
+// One CTA per (row block, axis): the three velocity updates are independent
+// (v_a needs only dp/dx_a, engine.hpp:275-283), so blockIdx.y selects the axis.
 template <int M, int N1, int RW>
 __global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zvel_fast_kernel(const __grid_constant__ ZvelFastArgs A) {
     using C = RowCfg<M, N1, RW>;
     constexpr int N2 = C::N2, TPR = C::TPR, NZ = C::NZ, NT = C::NT;
     extern __shared__ __align__(128) unsigned char sm_raw[];
     const GridDev& g = A.g;
+    const int a = blockIdx.y;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm_raw);
     float2* twM = reinterpret_cast<float2*>(sm_raw + 16);
     float2* zt = twM + M;
     float2* zn = zt + RW * C::ZT;
-    float2* sS = zn + RW * M;                       // [3][RW*nzp]
-    float* sV = reinterpret_cast<float*>(sS + 3 * RW * g.nzp);  // [3][RW*NZ]
-    float* sR = sV + 3 * RW * NZ;                   // [3][RW*NZ] (non-uniform dt/rho0~ only)
-    const bool coef_fields = A.r[0].field != nullptr;
+    float2* sS = zn + RW * M;                                   // [RW*nzp]
+    float* sV = reinterpret_cast<float*>(sS + RW * g.nzp);      // [RW*NZ]
+    float* sR = sV + RW * NZ;                                   // [RW*NZ] (non-uniform dt/rho0~ only)
+    const bool coef_field = A.r[a].field != nullptr;
+    float2* const Sa = A.S[a];
+    float* const va = A.v[a];
 
     const long long row0 = (long long)blockIdx.x * RW;
     const int nrows = (int)min((long long)RW, g.rows - row0);
     if (threadIdx.x == 0) mbar_init(bar, 1);
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned total = 3u * nrows * g.nzp * 8u + 3u * nrows * NZ * 4u + (coef_fields ? 3u * nrows * NZ * 4u : 0u);
+        const unsigned total = nrows * g.nzp * 8u + nrows * NZ * 4u + (coef_field ? nrows * NZ * 4u : 0u);
         mbar_arrive_expect_tx(bar, total);
         Stager st{bar};
-        for (int f = 0; f < 3; ++f) st.add(sS + f * RW * g.nzp, A.S[f] + row0 * g.nzp, nrows * g.nzp);
-        for (int f = 0; f < 3; ++f) st.add(sV + f * RW * NZ, A.v[f] + row0 * NZ, nrows * NZ);
-        if (coef_fields)
-            for (int f = 0; f < 3; ++f) st.add(sR + f * RW * NZ, A.r[f].field + row0 * NZ, nrows * NZ);
+        st.add(sS, Sa + row0 * g.nzp, nrows * g.nzp);
+        st.add(sV, va + row0 * NZ, nrows * NZ);
+        if (coef_field) st.add(sR, A.r[a].field + row0 * NZ, nrows * NZ);
     }
     for (int i = threadIdx.x; i < M; i += NT) twM[i] = g.pzh.tw[i];
     const int r = threadIdx.x / TPR, lane = threadIdx.x % TPR;
@@ -323,39 +411,36 @@ __global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zvel_fast_kernel(const 
     __syncthreads();
     mbar_wait(bar, 0);
 
-#pragma unroll 1
-    for (int a = 0; a < 3; ++a) {
-        if (rowok && lane < N1)
-            row_c2r_b<M, N1>(sS + a * RW * g.nzp + r * g.nzp, a == 2 ? A.dz_plus : nullptr, g.tw_rfft, twM, lane, zt_row);
-        __syncthreads();
-        float2 u[N1];
-        if (rowok && lane < N2) {
-            row_c2r_a<M, N1>(zt_row, lane, g.inv_n, u);
-            const float pa = a == 0 ? __ldg(A.pml.prof[0] + x) : (a == 1 ? __ldg(A.pml.prof[1] + y) : 0.f);
-            const float* vs = sV + a * RW * NZ + r * NZ;
-            const float* rs = sR + a * RW * NZ + r * NZ;
-            float* vg = A.v[a] + row * NZ;
+    if (rowok && lane < N1) row_c2r_b<M, N1>(sS + r * g.nzp, a == 2 ? A.dz_plus : nullptr, g.tw_rfft, twM, lane, zt_row);
+    __syncthreads();
+    float2 u[N1];
+    if (rowok && lane < N2) {
+        row_c2r_a<M, N1>(zt_row, lane, g.inv_n, u);
+        const float pa = a == 0 ? __ldg(A.pml.prof[0] + x) : (a == 1 ? __ldg(A.pml.prof[1] + y) : 0.f);
+        const float* vs = sV + r * NZ;
+        const float* rs = sR + r * NZ;
+        float* vg = va + row * NZ;
+        const float rsc = A.r[a].scalar;
 #pragma unroll
-            for (int n1 = 0; n1 < N1; ++n1) {
-                const int n = lane + N2 * n1;
-                float2 vv = *reinterpret_cast<const float2*>(vs + 2 * n);
-                float2 pm = make_float2(pa, pa);
-                if (a == 2) pm = make_float2(__ldg(A.pml.prof[2] + 2 * n), __ldg(A.pml.prof[2] + 2 * n + 1));
-                float2 rr = make_float2(A.r[a].scalar, A.r[a].scalar);
-                if (coef_fields) rr = *reinterpret_cast<const float2*>(rs + 2 * n);
-                vv.x = pm.x * (pm.x * vv.x - rr.x * u[n1].x);
-                vv.y = pm.y * (pm.y * vv.y - rr.y * u[n1].y);
-                *reinterpret_cast<float2*>(vg + 2 * n) = vv;
-                u[n1] = vv;
-            }
+        for (int n1 = 0; n1 < N1; ++n1) {
+            const int n = lane + N2 * n1;
+            float2 vv = *reinterpret_cast<const float2*>(vs + 2 * n);
+            float2 pm = make_float2(pa, pa);
+            if (a == 2) pm = *reinterpret_cast<const float2*>(A.pml.prof[2] + 2 * n);
+            float2 rr = make_float2(rsc, rsc);
+            if (coef_field) rr = *reinterpret_cast<const float2*>(rs + 2 * n);
+            vv.x = pm.x * (pm.x * vv.x - rr.x * u[n1].x);
+            vv.y = pm.y * (pm.y * vv.y - rr.y * u[n1].y);
+            *reinterpret_cast<float2*>(vg + 2 * n) = vv;
+            u[n1] = vv;
         }
-        __syncthreads();
-        if (rowok && lane < N2) row_r2c_a<M, N1>(u, lane, twM, zt_row);
-        __syncthreads();
-        if (rowok && lane < N1) row_r2c_b<M, N1>(zt_row, lane, zn_row);
-        __syncthreads();
-        if (rowok) row_r2c_finish<M, TPR>(zn_row, lane, g.tw_rfft, A.S[a] + row * g.nzp);
     }
+    __syncthreads();
+    if (rowok && lane < N2) row_r2c_a<M, N1>(u, lane, twM, zt_row);
+    __syncthreads();
+    if (rowok && lane < N1) row_r2c_b<M, N1>(zt_row, lane, zn_row);
+    __syncthreads();
+    if (rowok) row_r2c_finish<M, TPR>(zn_row, lane, g.tw_rfft, Sa + row * g.nzp);
 }
 
 struct ZrhoFastArgs {
@@ -363,25 +448,24 @@ struct ZrhoFastArgs {
     ZrhoArgs a;
 };
 
+// Density update of one axis per CTA (engine.hpp:284-291): c2r of dv_a/dx_a (D_z- on z),
+// rho_a = pml_a (pml_a rho_a - dt rho0 dv_a), written back. The three axes are independent.
 template <int M, int N1, int RW>
-__global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zrho_fast_kernel(const __grid_constant__ ZrhoFastArgs P) {
+__global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zrho_axis_kernel(const __grid_constant__ ZrhoFastArgs P) {
     using C = RowCfg<M, N1, RW>;
     constexpr int N2 = C::N2, TPR = C::TPR, NZ = C::NZ, NT = C::NT;
     extern __shared__ __align__(128) unsigned char sm_raw[];
     const GridDev& g = P.g;
     const ZrhoArgs& A = P.a;
+    const int a = blockIdx.y;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm_raw);
     float2* twM = reinterpret_cast<float2*>(sm_raw + 16);
     float2* zt = twM + M;
-    float2* zn = zt + RW * C::ZT;
-    float2* sS = zn + RW * M;                                   // [3][RW*nzp]
-    float* sR = reinterpret_cast<float*>(sS + 3 * RW * g.nzp);  // [3][RW*NZ] rho
-    float* sC = sR + 3 * RW * NZ;                               // c0^2
+    float2* sS = zt + RW * C::ZT;                              // [RW*nzp]
+    float* sR = reinterpret_cast<float*>(sS + RW * g.nzp);     // [RW*NZ] rho_a
+    float* sD = sR + RW * NZ;                                  // dt*rho0 field (optional)
     const bool coef_field = A.dtrho0.field != nullptr;
-    const bool corr = A.corr.grad != nullptr;
-    float* sD = sC + RW * NZ;                                   // dt*rho0 field (optional)
-    float* sK = sC + (coef_field ? 2 : 1) * RW * NZ;            // correlation: p_mid, p_old, q_adj, grad
-    __shared__ int sp[8];
+    float* const ra = A.rho[a];
 
     const long long row0 = (long long)blockIdx.x * RW;
     const int nrows = (int)min((long long)RW, g.rows - row0);
@@ -389,23 +473,69 @@ __global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zrho_fast_kernel(const 
     if (threadIdx.x == 0) mbar_init(bar, 1);
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned fb = nrows * NZ * 4u;
-        unsigned total = 3u * nrows * g.nzp * 8u + 4u * fb + (coef_field ? fb : 0u) + (corr ? 4u * fb : 0u);
+        const unsigned total = nrows * g.nzp * 8u + nrows * NZ * 4u + (coef_field ? nrows * NZ * 4u : 0u);
         mbar_arrive_expect_tx(bar, total);
         Stager st{bar};
-        for (int f = 0; f < 3; ++f) st.add(sS + f * RW * g.nzp, A.S[f] + row0 * g.nzp, nrows * g.nzp);
-        for (int f = 0; f < 3; ++f) st.add(sR + f * RW * NZ, A.rho[f] + i0, nrows * NZ);
-        st.add(sC, A.c0sq + i0, nrows * NZ);
+        st.add(sS, A.S[a] + row0 * g.nzp, nrows * g.nzp);
+        st.add(sR, ra + i0, nrows * NZ);
         if (coef_field) st.add(sD, A.dtrho0.field + i0, nrows * NZ);
-        if (corr) {
-            st.add(sK, A.corr.p_mid + i0, nrows * NZ);
-            st.add(sK + RW * NZ, A.corr.p_old + i0, nrows * NZ);
-            st.add(sK + 2 * RW * NZ, A.corr.q_adj + i0, nrows * NZ);
-            st.add(sK + 3 * RW * NZ, A.corr.grad + i0, nrows * NZ);
+    }
+    for (int i = threadIdx.x; i < M; i += NT) twM[i] = g.pzh.tw[i];
+    const int r = threadIdx.x / TPR, lane = threadIdx.x % TPR;
+    const bool rowok = r < nrows;
+    const long long row = row0 + r;
+    const int x = rowok ? (int)(row / g.ny) : 0, y = rowok ? (int)(row % g.ny) : 0;
+    float2* zt_row = zt + r * C::ZT;
+    __syncthreads();
+    mbar_wait(bar, 0);
+
+    if (rowok && lane < N1) row_c2r_b<M, N1>(sS + r * g.nzp, a == 2 ? A.dz_minus : nullptr, g.tw_rfft, twM, lane, zt_row);
+    __syncthreads();
+    if (rowok && lane < N2) {
+        float2 u[N1];
+        row_c2r_a<M, N1>(zt_row, lane, g.inv_n, u);
+        const float pa = a == 0 ? __ldg(A.pml.prof[0] + x) : (a == 1 ? __ldg(A.pml.prof[1] + y) : 0.f);
+        const float* rs = sR + r * NZ;
+        const float* ds = sD + r * NZ;
+        float* rg = ra + row * NZ;
+        const float dsc = A.dtrho0.scalar;
+#pragma unroll
+        for (int n1 = 0; n1 < N1; ++n1) {
+            const int n = lane + N2 * n1;
+            float2 q = *reinterpret_cast<const float2*>(rs + 2 * n);
+            float2 pm = make_float2(pa, pa);
+            if (a == 2) pm = *reinterpret_cast<const float2*>(A.pml.prof[2] + 2 * n);
+            float2 d = make_float2(dsc, dsc);
+            if (coef_field) d = *reinterpret_cast<const float2*>(ds + 2 * n);
+            q.x = pm.x * (pm.x * q.x - d.x * u[n1].x);
+            q.y = pm.y * (pm.y * q.y - d.y * u[n1].y);
+            *reinterpret_cast<float2*>(rg + 2 * n) = q;
         }
     }
-    if (threadIdx.x == 32 % NT) {
-        const int lo_key = (int)i0, hi_key = (int)(i0 + (long long)nrows * NZ);
+}
+
+// Pressure step (update_pressure, engine.hpp:318-326) with the sparse work that sits between
+// the density update and p (mass sources :296-300 / shell Dirichlet :304-307), the gathers
+// (simulate.hpp:88-95), the TR correlation (gradient.hpp:177-182) and the r2c of p.
+// Thread (row, n2) owns the pairs n = n2 + N2*n1 of its row in registers; sparse entries
+// are applied by the owner thread.
+template <int M, int N1, int RW>
+__global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zp_kernel(const __grid_constant__ ZrhoFastArgs P) {
+    using C = RowCfg<M, N1, RW>;
+    constexpr int N2 = C::N2, TPR = C::TPR, NZ = C::NZ, NT = C::NT;
+    extern __shared__ __align__(128) unsigned char sm_raw[];
+    const GridDev& g = P.g;
+    const ZrhoArgs& A = P.a;
+    float2* twM = reinterpret_cast<float2*>(sm_raw + 16);
+    float2* zt = twM + M;
+    float2* zn = zt + RW * C::ZT;
+    __shared__ int sp[8];
+    const long long row0 = (long long)blockIdx.x * RW;
+    const int nrows = (int)min((long long)RW, g.rows - row0);
+    const long long i0 = row0 * NZ;
+    const int lo_key = (int)i0;
+    if (threadIdx.x == 0) {
+        const int hi_key = (int)(i0 + (long long)nrows * NZ);
         auto lb = [](const int* a, int n, int key) {
             int lo = 0, hi = n;
             while (lo < hi) {
@@ -427,100 +557,104 @@ __global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zrho_fast_kernel(const 
     for (int i = threadIdx.x; i < M; i += NT) twM[i] = g.pzh.tw[i];
     const int r = threadIdx.x / TPR, lane = threadIdx.x % TPR;
     const bool rowok = r < nrows;
-    const long long row = row0 + r;
     const bool act = rowok && lane < N2;
-    const int x = rowok ? (int)(row / g.ny) : 0, y = rowok ? (int)(row % g.ny) : 0;
+    const long long row = row0 + r;
     float2* zt_row = zt + r * C::ZT;
     float2* zn_row = zn + r * M;
-    __syncthreads();
-    mbar_wait(bar, 0);
 
-    // density updates, written back in place into sR
-#pragma unroll 1
-    for (int a = 0; a < 3; ++a) {
-        if (rowok && lane < N1)
-            row_c2r_b<M, N1>(sS + a * RW * g.nzp + r * g.nzp, a == 2 ? A.dz_minus : nullptr, g.tw_rfft, twM, lane, zt_row);
-        __syncthreads();
-        if (act) {
-            float2 u[N1];
-            row_c2r_a<M, N1>(zt_row, lane, g.inv_n, u);
-            const float pa = a == 0 ? __ldg(A.pml.prof[0] + x) : (a == 1 ? __ldg(A.pml.prof[1] + y) : 0.f);
-            float* rs = sR + a * RW * NZ + r * NZ;
-            const float* ds = sD + r * NZ;
+    // all global loads of this thread's pairs first (memory-level parallelism)
+    float2 q0[N1], q1[N1], q2[N1], c2[N1];
+    if (act) {
 #pragma unroll
-            for (int n1 = 0; n1 < N1; ++n1) {
-                const int n = lane + N2 * n1;
-                float2 q = *reinterpret_cast<float2*>(rs + 2 * n);
-                float2 pm = make_float2(pa, pa);
-                if (a == 2) pm = make_float2(__ldg(A.pml.prof[2] + 2 * n), __ldg(A.pml.prof[2] + 2 * n + 1));
-                float2 d = make_float2(A.dtrho0.scalar, A.dtrho0.scalar);
-                if (coef_field) d = *reinterpret_cast<const float2*>(ds + 2 * n);
-                q.x = pm.x * (pm.x * q.x - d.x * u[n1].x);
-                q.y = pm.y * (pm.y * q.y - d.y * u[n1].y);
-                *reinterpret_cast<float2*>(rs + 2 * n) = q;
-            }
+        for (int n1 = 0; n1 < N1; ++n1) {
+            const long long i = row * NZ + 2 * (lane + N2 * n1);
+            q0[n1] = *reinterpret_cast<const float2*>(A.rho[0] + i);
+            q1[n1] = *reinterpret_cast<const float2*>(A.rho[1] + i);
+            q2[n1] = *reinterpret_cast<const float2*>(A.rho[2] + i);
+            c2[n1] = *reinterpret_cast<const float2*>(A.c0sq + i);
         }
-        __syncthreads();
     }
+    __syncthreads();  // sp[] ready
 
-    // sparse mass sources / Dirichlet shell on the split densities (after the update, before p)
-    const int lo_key = (int)i0;
-    for (int u = sp[0] + threadIdx.x; u < sp[1]; u += NT) {
-        const int t = A.inj.pos[u] - lo_key;
+    // sparse sources / shell, applied by the owner of each position
+    bool modified = false;
+    auto owner_apply = [&](int pos, auto&& fn) {
+        const int t = pos - lo_key;
+        const int rr = t / NZ, z = t % NZ, n = z >> 1, comp = z & 1;
+        if (!(act && rr == r && (n % N2) == lane)) return;
+        const int n1 = n / N2;
+#pragma unroll
+        for (int k = 0; k < N1; ++k)
+            if (k == n1) fn(k, comp);
+    };
+    auto set_rho = [&](int k, int comp, float v, bool add) {
+        auto upd = [&](float2& q) {
+            float& s = comp ? q.y : q.x;
+            s = add ? s + v : v;
+        };
+        if (A.a_first <= 0) upd(q0[k]);
+        if (A.a_first <= 1) upd(q1[k]);
+        upd(q2[k]);
+    };
+    for (int u = sp[0]; u < sp[1]; ++u) {
+        const int pos = A.inj.pos[u];
         const float sc = A.inj.scale[u];
         for (int cc = A.inj.csr[u]; cc < A.inj.csr[u + 1]; ++cc) {
             const int n = A.step_n - A.inj.delay[cc];
             if (n < 0 || n >= A.inj.len[cc]) continue;
             const float amp = A.inj.w[cc] * A.inj.sig[A.inj.off[cc] + (long long)n * A.inj.stride[cc]];
             if (amp == 0.f) continue;
-            for (int a = A.a_first; a < 3; ++a) sR[a * RW * NZ + t] += amp * sc;
+            owner_apply(pos, [&](int k, int comp) {
+                set_rho(k, comp, amp * sc, true);
+                modified = true;
+            });
         }
     }
-    for (int j = sp[2] + threadIdx.x; j < sp[3]; j += NT) {
-        const int t = A.enf.pos[j] - lo_key;
-        const float val = A.enf.vals[j] / (A.enf.ndim * sC[t]);
-        for (int a = A.a_first; a < 3; ++a) sR[a * RW * NZ + t] = val;
+    for (int j = sp[2]; j < sp[3]; ++j) {
+        const int pos = A.enf.pos[j];
+        owner_apply(pos, [&](int k, int comp) {
+            const float c2v = comp ? c2[k].y : c2[k].x;
+            set_rho(k, comp, A.enf.vals[j] / (A.enf.ndim * c2v), false);
+            modified = true;
+        });
     }
-    __syncthreads();
 
-    // p = c0^2 ((rho_x + rho_y) + rho_z); stores; correlation; p kept in sR[0] for gathers + r2c
     float2 pv[N1];
     if (act) {
-        float* gr = A.corr.grad;
 #pragma unroll
         for (int n1 = 0; n1 < N1; ++n1) {
-            const int n = lane + N2 * n1;
-            const int t = r * NZ + 2 * n;
-            const long long i = i0 + t;
-            const float2 q0 = *reinterpret_cast<const float2*>(sR + t);
-            const float2 q1 = *reinterpret_cast<const float2*>(sR + RW * NZ + t);
-            const float2 q2 = *reinterpret_cast<const float2*>(sR + 2 * RW * NZ + t);
-            *reinterpret_cast<float2*>(A.rho[0] + i) = q0;
-            *reinterpret_cast<float2*>(A.rho[1] + i) = q1;
-            *reinterpret_cast<float2*>(A.rho[2] + i) = q2;
-            const float2 c2 = *reinterpret_cast<const float2*>(sC + t);
-            float2 p;
-            p.x = c2.x * ((q0.x + q1.x) + q2.x);
-            p.y = c2.y * ((q0.y + q1.y) + q2.y);
-            *reinterpret_cast<float2*>(A.p_out + i) = p;
-            *reinterpret_cast<float2*>(sR + t) = p;
-            if (corr) {
-                const float2 pm = *reinterpret_cast<const float2*>(sK + t);
-                const float2 po = *reinterpret_cast<const float2*>(sK + RW * NZ + t);
-                const float2 qa = *reinterpret_cast<const float2*>(sK + 2 * RW * NZ + t);
-                float2 gv = *reinterpret_cast<const float2*>(sK + 3 * RW * NZ + t);
-                const float wx = 2.f / (c2.x * sqrtf(c2.x)), wy = 2.f / (c2.y * sqrtf(c2.y));
-                gv.x += wx * (((p.x - 2.f * pm.x) + po.x) * A.corr.inv_dt) * qa.x;
-                gv.y += wy * (((p.y - 2.f * pm.y) + po.y) * A.corr.inv_dt) * qa.y;
-                *reinterpret_cast<float2*>(gr + i) = gv;
+            const long long i = row * NZ + 2 * (lane + N2 * n1);
+            if (modified) {
+                *reinterpret_cast<float2*>(A.rho[0] + i) = q0[n1];
+                *reinterpret_cast<float2*>(A.rho[1] + i) = q1[n1];
+                *reinterpret_cast<float2*>(A.rho[2] + i) = q2[n1];
             }
-            if (A.check_step > 0 && i == 0 && !isfinite(p.x)) atomicMin(A.diverged, A.check_step);
+            float2 p;
+            p.x = c2[n1].x * ((q0[n1].x + q1[n1].x) + q2[n1].x);
+            p.y = c2[n1].y * ((q0[n1].y + q1[n1].y) + q2[n1].y);
+            *reinterpret_cast<float2*>(A.p_out + i) = p;
             pv[n1] = p;
         }
+        if (A.corr.grad != nullptr) {
+#pragma unroll
+            for (int n1 = 0; n1 < N1; ++n1) {
+                const long long i = row * NZ + 2 * (lane + N2 * n1);
+                const float2 pm = *reinterpret_cast<const float2*>(A.corr.p_mid + i);
+                const float2 po = *reinterpret_cast<const float2*>(A.corr.p_old + i);
+                const float2 qa = *reinterpret_cast<const float2*>(A.corr.q_adj + i);
+                float2 gv = *reinterpret_cast<const float2*>(A.corr.grad + i);
+                const float wx = 2.f / (c2[n1].x * sqrtf(c2[n1].x)), wy = 2.f / (c2[n1].y * sqrtf(c2[n1].y));
+                gv.x += wx * (((pv[n1].x - 2.f * pm.x) + po.x) * A.corr.inv_dt) * qa.x;
+                gv.y += wy * (((pv[n1].y - 2.f * pm.y) + po.y) * A.corr.inv_dt) * qa.y;
+                *reinterpret_cast<float2*>(A.corr.grad + i) = gv;
+            }
+        }
+        if (A.check_step > 0 && row == 0 && lane == 0 && !isfinite(pv[0].x)) atomicMin(A.diverged, A.check_step);
     }
-    __syncthreads();
-    for (int s = sp[4] + threadIdx.x; s < sp[5]; s += NT) A.sens.out[A.sens.idx[s]] = sR[A.sens.pos[s] - lo_key];
-    for (int j = sp[6] + threadIdx.x; j < sp[7]; j += NT) A.shell.out[j] = sR[A.shell.pos[j] - lo_key];
+    for (int s = sp[4]; s < sp[5]; ++s)
+        owner_apply(A.sens.pos[s], [&](int k, int comp) { A.sens.out[A.sens.idx[s]] = comp ? pv[k].y : pv[k].x; });
+    for (int j = sp[6]; j < sp[7]; ++j)
+        owner_apply(A.shell.pos[j], [&](int k, int comp) { A.shell.out[j] = comp ? pv[k].y : pv[k].x; });
 
     // forward r2c of p into S0
     if (act) row_r2c_a<M, N1>(pv, lane, twM, zt_row);
@@ -535,24 +669,45 @@ __global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zrho_fast_kernel(const 
 // ======================================================================================
 namespace {
 
-template <int AXIS, bool INV, int L, int N1, int TB, int MINB>
+int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <int AXIS, bool INV, int L, int N1, int TB, int MINB, bool DB>
 cudaError_t run_pencil(const GridDev& g, const PencilJobs& j, cudaStream_t st) {
-    using C = PencilCfg<L, N1, TB>;
-    auto kern = pencil_fast_kernel<AXIS, INV, L, N1, TB, MINB>;
+    using C = PencilCfg<L, N1, TB, DB>;
+    auto kern = pencil_fast_kernel<AXIS, INV, L, N1, TB, MINB, DB>;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
         configured = true;
     }
-    dim3 grid((g.nzh + TB - 1) / TB, AXIS == 0 ? g.ny : g.nx);
+    const int ntiles = ((g.nzh + TB - 1) / TB) * (AXIS == 0 ? g.ny : g.nx);
+    const int grid = (!DB || ntiles < sm_count() * MINB) ? ntiles : sm_count() * MINB;
     kern<<<grid, C::NT, C::SMEM, st>>>(g, j);
     return cudaGetLastError();
 }
 
-template <int L, int N1, int TB, int MINB>
+template <int L, int N1, int TB, int MINB, bool DB>
 cudaError_t pencil_sized(int axis, bool inv, const GridDev& g, const PencilJobs& j, cudaStream_t st) {
-    if (axis == 0) return run_pencil<0, false, L, N1, TB, MINB>(g, j, st);
-    return inv ? run_pencil<1, true, L, N1, TB, MINB>(g, j, st) : run_pencil<1, false, L, N1, TB, MINB>(g, j, st);
+    if (axis == 0) return run_pencil<0, false, L, N1, TB, MINB, DB>(g, j, st);
+    return inv ? run_pencil<1, true, L, N1, TB, MINB, DB>(g, j, st)
+               : run_pencil<1, false, L, N1, TB, MINB, DB>(g, j, st);
+}
+
+bool pencil_double_buffer() {
+    static const bool db = [] {
+        const char* e = getenv("USTFWI_PENCIL_DB");  // default on; "0" selects single buffering
+        return !(e && e[0] == '0');
+    }();
+    return db;
 }
 
 }  // namespace
@@ -567,13 +722,15 @@ bool fast_pencil_supported(int L) {
 cudaError_t launch_pencil_fast(int axis, bool inv, const GridDev& g, const PencilJobs& j, cudaStream_t st) {
     const int L = axis == 0 ? g.px.L : g.py.L;
     switch (L) {
-        case 32: return pencil_sized<32, 2, 16, 4>(axis, inv, g, j, st);
-        case 64: return pencil_sized<64, 4, 16, 4>(axis, inv, g, j, st);
-        case 96: return pencil_sized<96, 6, 16, 4>(axis, inv, g, j, st);
-        case 128: return pencil_sized<128, 8, 16, 4>(axis, inv, g, j, st);
-        case 144: return pencil_sized<144, 9, 16, 3>(axis, inv, g, j, st);
-        case 256: return pencil_sized<256, 16, 16, 3>(axis, inv, g, j, st);
-        case 480: return pencil_sized<480, 30, 8, 3>(axis, inv, g, j, st);
+        case 32: return pencil_sized<32, 2, 16, 4, false>(axis, inv, g, j, st);
+        case 64: return pencil_sized<64, 4, 16, 4, false>(axis, inv, g, j, st);
+        case 96: return pencil_sized<96, 6, 16, 3, false>(axis, inv, g, j, st);
+        case 128: return pencil_sized<128, 8, 16, 3, false>(axis, inv, g, j, st);
+        case 144: return pencil_sized<144, 16, 16, 3, false>(axis, inv, g, j, st);
+        case 256: return pencil_sized<256, 16, 16, 3, false>(axis, inv, g, j, st);
+        case 480:
+            return pencil_double_buffer() ? pencil_sized<480, 32, 8, 2, true>(axis, inv, g, j, st)
+                                          : pencil_sized<480, 32, 8, 3, false>(axis, inv, g, j, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -601,11 +758,10 @@ cudaError_t zvel_sized(const GridDev& g, float2* S[3], const float2* dz_plus, fl
     }
     a.dz_plus = dz_plus;
     a.pml = pml;
-    const size_t smem = C::FIXED + size_t(3) * kZRows * g.nzp * 8 +
-                        size_t(r[0].field ? 6 : 3) * kZRows * C::NZ * 4;
+    const size_t smem = C::FIXED + size_t(kZRows) * g.nzp * 8 + size_t(r[0].field ? 2 : 1) * kZRows * C::NZ * 4;
     auto kern = zvel_fast_kernel<M, N1, kZRows>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const unsigned blocks = (unsigned)((g.rows + kZRows - 1) / kZRows);
+    const dim3 blocks((unsigned)((g.rows + kZRows - 1) / kZRows), 3);
     kern<<<blocks, C::NT, smem, st>>>(a);
     return cudaGetLastError();
 }
@@ -615,12 +771,19 @@ cudaError_t zrho_sized(const GridDev& g, const ZrhoArgs& za, cudaStream_t st) {
     ZrhoFastArgs a;
     a.g = g;
     a.a = za;
-    const int nf = 4 + (za.dtrho0.field ? 1 : 0) + (za.corr.grad ? 4 : 0);
-    const size_t smem = C::FIXED + size_t(3) * kZRows * g.nzp * 8 + size_t(nf) * kZRows * C::NZ * 4;
-    auto kern = zrho_fast_kernel<M, N1, kZRows>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const unsigned blocks = (unsigned)((g.rows + kZRows - 1) / kZRows);
-    kern<<<blocks, C::NT, smem, st>>>(a);
+    // density update, one CTA per (row block, axis)
+    const size_t smem1 = 16 + size_t(M) * 8 + size_t(kZRows) * C::ZT * 8 + size_t(kZRows) * g.nzp * 8 +
+                         size_t(za.dtrho0.field ? 2 : 1) * kZRows * C::NZ * 4;
+    auto k1 = zrho_axis_kernel<M, N1, kZRows>;
+    cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+    k1<<<dim3(blocks, 3), C::NT, smem1, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // pressure, sparse work, gathers, correlation, r2c of p
+    const size_t smem2 = C::FIXED;
+    auto k2 = zp_kernel<M, N1, kZRows>;
+    k2<<<blocks, C::NT, smem2, st>>>(a);
     return cudaGetLastError();
 }
 }  // namespace
