@@ -35,6 +35,17 @@ BYTES_PER_VU_MODEL = 128.0   # B_step per voxel-update (fp32, 
 BYTES_CORR_MODEL = 16.0      # per voxel per adjoint+TR pair-step
 
 
+def ncu_traffic(config_name: str, kernel_class: str):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, averaged over the
+    launches of the class) from the committed ncu launch list of this config, if any."""
+    p = os.path.join(ROOT, "profiles", f"r1_launches_config{config_name}.json")
+    try:
+        d = json.load(open(p))
+        return float(d["class_dram_bytes_per_launch_avg"][kernel_class]), os.path.relpath(p, ROOT)
+    except Exception:
+        return None, None
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -241,7 +252,6 @@ def b200_arm(a):
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    eng.set_profiling(True)
     l0 = eng.launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -258,7 +268,12 @@ def b200_arm(a):
         if world > 1:
             dist.barrier()
     launches = eng.launch_count() - l0
+    # per-launch-class CUDA-event timing: one extra gradient with profiling on (the engine
+    # then serialises adjoint and replay on one stream so each launch is timed alone)
+    eng.set_profiling(True)
+    eng.run_gradient(sc.thickness)
     stats = eng.kernel_stats()
+    prof_ms = sum(v[0] for v in stats.values())
     eng.set_profiling(False)
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], dtype=torch.float64)
@@ -304,10 +319,11 @@ def b200_arm(a):
     dom = max(stats, key=lambda k: stats[k][0])
     d_ms, d_n, d_b = stats[dom]
     achieved = (d_b / d_n) / (d_ms / d_n / 1e3) / 1e9 if d_n else 0.0
+    traffic, traffic_src = ncu_traffic(sc.name, dom)
     kernels = {k: {"ms_total": v[0], "launches": v[1], "ms_per_launch": v[0] / v[1] if v[1] else 0.0,
                    "GB_per_launch": v[2] / v[1] / 1e9 if v[1] else 0.0,
                    "achieved_GBps": (v[2] / v[0] * 1e3 / 1e9) if v[0] else 0.0,
-                   "share_of_step": v[0] / ms if ms else 0.0} for k, v in stats.items() if v[1]}
+                   "share_of_profiled_gradient": v[0] / prof_ms if prof_ms else 0.0} for k, v in stats.items() if v[1]}
     n = g.points
     b_model = n * (BYTES_PER_VU_MODEL * (3 * g.nt - 3) + BYTES_CORR_MODEL * (g.nt - 2))
     path_gbps = b_model / s_per_step / 1e9
@@ -321,12 +337,14 @@ def b200_arm(a):
         "s_per_gradient": s_per_step,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "peak_kind": peak_kind,
-                     "traffic": None,
+                     "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": d_b / d_n if d_n else 0.0},
         "path_roofline": {"model_bytes_per_gradient": b_model, "model_B_per_voxel_update": b_model / vu,
                           "achieved_GBps": path_gbps, "frac_of_measured": path_gbps / hbm,
                           "frac_of_8TBps": path_gbps / 8000.0},
         "kernels": kernels,
+        "kernel_timing": "CUDA events around every launch of one extra gradient after the timed region "
+                         "(adjoint and replay serialised on one stream for that gradient)",
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "e2e": e2e,

@@ -104,6 +104,9 @@ NcclApi& nccl() {
 struct ustfwi_gpu_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t stream2 = nullptr;   // time-reversal replay stream of the pair loop
+    cudaEvent_t ev_adj[2] = {}, ev_rep[2] = {}, ev_fork = nullptr, ev_join = nullptr;
+    float* adj_p2 = nullptr;          // second adjoint pressure buffer (pair loop)
     uint64_t launches = 0;
     ustfwi_grid grid{};
     int ndim = 3;
@@ -178,15 +181,15 @@ struct ustfwi_gpu_ctx {
         return e;
     }
     template <class F>
-    void launch(int kind, double bytes, F&& f) {
+    void launch(int kind, double bytes, F&& f, cudaStream_t st) {
         if (!profiling) {
             count(f());
             return;
         }
         Pending pd{get_event(), get_event(), kind, bytes};
-        CK(cudaEventRecord(pd.a, stream));
+        CK(cudaEventRecord(pd.a, st));
         count(f());
-        CK(cudaEventRecord(pd.b, stream));
+        CK(cudaEventRecord(pd.b, st));
         pending.push_back(pd);
         if (pending.size() > 4096) resolve_profile();
     }
@@ -285,11 +288,12 @@ struct StepIO {
     int step_n = 0;
     int check_step = 0;
     float* p_out = nullptr;
+    cudaEvent_t wait_before_z = nullptr;  // cross-stream dependency of the pressure kernel
 };
 
 // One leapfrog step of a stepper: update_velocity_density (engine.hpp:270-292), sparse
 // injection / shell enforcement, update_pressure (:318-347), gathers — 8 launches.
-void run_step(Ctx& c, Sim& s, const StepIO& io) {
+void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     const GridDev& g = c.g;
     const double SB = static_cast<double>(g.rows) * g.nzh * sizeof(float2);  // one half spectrum
     const double FB = static_cast<double>(g.N) * sizeof(float);               // one real field
@@ -297,8 +301,7 @@ void run_step(Ctx& c, Sim& s, const StepIO& io) {
         int loads = 0;
         for (int q = 0; q < j.n; ++q)
             if (q == 0 || j.job[q].src != j.job[q - 1].src) ++loads;
-        c.launch(axis == 0 ? KIND_X : KIND_Y, (loads + j.n) * SB,
-                 [&] { return launch_pencil(axis, inv, g, j, c.stream); });
+        c.launch(axis == 0 ? KIND_X : KIND_Y, (loads + j.n) * SB, [&] { return launch_pencil(axis, inv, g, j, st); }, st);
     };
     PencilJobs j{};
     for (int f = 0; f < 3; ++f) j.buf[f] = s.S[f];
@@ -321,7 +324,7 @@ void run_step(Ctx& c, Sim& s, const StepIO& io) {
     Pml ps{{c.pml_stag[0], c.pml_stag[1], c.pml_stag[2]}};
     const double coef_b = c.dtr_stag[0].field ? 3 * FB : 0.0;
     c.launch(KIND_ZVEL, 6 * SB + 6 * FB + coef_b,
-             [&] { return launch_zvel(g, s.S, c.dmul[2][ST_PLUS], s.v, ps, c.dtr_stag, c.stream); });
+             [&] { return launch_zvel(g, s.S, c.dmul[2][ST_PLUS], s.v, ps, c.dtr_stag, st); }, st);
     // Y forward x3
     j.n = 3;
     for (int f = 0; f < 3; ++f) j.job[f] = {f, f, nullptr, 0};
@@ -360,7 +363,8 @@ void run_step(Ctx& c, Sim& s, const StepIO& io) {
     // kernel, which re-reads the three split densities (+3F)
     const bool split = !use_generic_kernels() && fast_rows_supported(g.nz);
     const double zb = 4 * SB + (split ? 11 : 8) * FB + (c.dtrho0.field ? FB : 0.0) + (io.corr.grad ? 5 * FB : 0.0);
-    c.launch(KIND_ZRHO, zb, [&] { return launch_zrho(g, a, true, c.stream); });
+    if (io.wait_before_z) CK(cudaStreamWaitEvent(st, io.wait_before_z, 0));
+    c.launch(KIND_ZRHO, zb, [&] { return launch_zrho(g, a, true, st); }, st);
     if (split) ++c.launches;
 }
 
@@ -481,7 +485,7 @@ void forward_sim(Ctx& c, int thickness) {
         io.sens.out = c.data + static_cast<size_t>(n) * c.n_sens;
         if (n_shell) io.shell.out = c.trace + static_cast<size_t>(n) * n_shell;
         io.check_step = ((n + 1) & 63) == 0 ? n + 1 : 0;
-        run_step(c, s, io);
+        run_step(c, s, io, c.stream);
     }
     if (c.n_sens > 0) c.count(launch_check_finite(c.data, static_cast<long long>(nt) * c.n_sens, c.flags + 2, c.stream));
 }
@@ -507,6 +511,19 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
     const int n_shell = static_cast<int>(c.shell_host.size());
     auto shell_row = [&](int m) { return c.trace + static_cast<size_t>(m) * n_shell; };
 
+    // The adjoint runs on c.stream and the time-reversal replay on c.stream2, so their
+    // passes overlap; the only coupling is the correlation in the replay's pressure kernel
+    // (reads the adjoint pressure of the same pair step). The adjoint pressure is double
+    // buffered: adjoint step n writes P[n&1] once replay step n-2 (its last reader) is done.
+    // Profiling serialises both on one stream so per-launch event times stay meaningful.
+    const bool dual = !c.profiling && c.stream2 != nullptr;
+    cudaStream_t sa = c.stream, sb = dual ? c.stream2 : c.stream;
+    float* P[2] = {adj.p, c.adj_p2};
+    if (dual) {
+        CK(cudaEventRecord(c.ev_fork, sa));
+        CK(cudaStreamWaitEvent(sb, c.ev_fork, 0));
+    }
+
     // replay initial value: enforce g[last], refresh p (gradient.hpp:435-437)
     {
         ZrhoArgs a{};
@@ -521,28 +538,36 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
         a.a_first = c.off_axis;
         a.enf = SparseEnforce{n_shell, c.shell_pos, shell_row(last), static_cast<float>(c.ndim)};
         a.diverged = c.flags;
-        c.count(launch_zrho(c.g, a, false, c.stream));
+        c.count(launch_zrho(c.g, a, false, sb));
     }
     // look-ahead step (gradient.hpp:438-441)
     StepIO rio;
     rio.enf = SparseEnforce{n_shell, c.shell_pos, shell_row(last - 1), static_cast<float>(c.ndim)};
     rio.p_out = c.ring[1];
     rio.check_step = 0;
-    run_step(c, rep, rio);
+    run_step(c, rep, rio, sb);
 
     StepIO aio;
     aio.inj = c.adj.view(c.q);
-    aio.p_out = adj.p;
     const float inv_dt = static_cast<float>(1.0 / c.grid.dt);
     for (int n = 1; n <= last - 1; ++n) {
         aio.step_n = n;
         aio.check_step = (n & 63) == 0 ? n : 0;
-        run_step(c, adj, aio);
+        aio.p_out = P[n & 1];
+        aio.wait_before_z = (dual && n >= 3) ? c.ev_rep[n & 1] : nullptr;  // replay n-2 done with P[n&1]
+        run_step(c, adj, aio, sa);
+        if (dual) CK(cudaEventRecord(c.ev_adj[n & 1], sa));
         rio.enf.vals = shell_row(last - n - 1);
         rio.p_out = c.ring[(n + 1) % 3];
-        rio.corr = Correlate{c.ring[n % 3], c.ring[(n - 1) % 3], adj.p, c.grad, inv_dt};
+        rio.corr = Correlate{c.ring[n % 3], c.ring[(n - 1) % 3], P[n & 1], c.grad, inv_dt};
         rio.check_step = ((n + 1) & 63) == 0 ? n + 1 : 0;
-        run_step(c, rep, rio);
+        rio.wait_before_z = dual ? c.ev_adj[n & 1] : nullptr;                 // adjoint step n done
+        run_step(c, rep, rio, sb);
+        if (dual) CK(cudaEventRecord(c.ev_rep[n & 1], sb));
+    }
+    if (dual) {
+        CK(cudaEventRecord(c.ev_join, sb));
+        CK(cudaStreamWaitEvent(sa, c.ev_join, 0));
     }
     c.count(launch_finalize_grad(c.grad, c.gamma, c.g.N, c.acc, accumulate ? 1 : 0, c.flags + 1, c.stream));
 }
@@ -614,6 +639,13 @@ int ustfwi_gpu_create(int device, const ustfwi_grid* grid, ustfwi_gpu_ctx** out)
         if (prop.major < 10)
             fail(USTFWI_ERR_CUDA, std::string("device ") + prop.name + " is not sm_100-class (built for sm_100a)");
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k) {
+            CK(cudaEventCreateWithFlags(&c->ev_adj[k], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_rep[k], cudaEventDisableTiming));
+        }
+        CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         c->grid = *grid;
         c->ndim = grid->ndim;
         c->off_axis = 3 - grid->ndim;
@@ -700,6 +732,7 @@ int ustfwi_gpu_create(int device, const ustfwi_grid* grid, ustfwi_gpu_ctx** out)
             }
         }
         c->sim[0].p = c->alloc<float>(N);
+        c->adj_p2 = c->alloc<float>(N);
         for (int r = 0; r < 3; ++r) c->ring[r] = c->alloc<float>(N);
         c->grad = c->alloc<float>(N);
         c->acc = c->alloc<float>(N);
@@ -735,7 +768,13 @@ void ustfwi_gpu_destroy(ustfwi_gpu_ctx* c) {
         c->event_pool.push_back(pd.b);
     }
     for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : {c->ev_adj[0], c->ev_adj[1], c->ev_rep[0], c->ev_rep[1], c->ev_fork, c->ev_join})
+        if (e) cudaEventDestroy(e);
     for (void* p : c->allocs) cudaFree(p);
+    if (c->stream2) {
+        cudaStreamSynchronize(c->stream2);
+        cudaStreamDestroy(c->stream2);
+    }
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
