@@ -702,14 +702,6 @@ cudaError_t pencil_sized(int axis, bool inv, const GridDev& g, const PencilJobs&
                : run_pencil<1, false, L, N1, TB, MINB, DB>(g, j, st);
 }
 
-bool pencil_double_buffer() {
-    static const bool db = [] {
-        const char* e = getenv("USTFWI_PENCIL_DB");  // default on; "0" selects single buffering
-        return !(e && e[0] == '0');
-    }();
-    return db;
-}
-
 }  // namespace
 
 bool fast_pencil_supported(int L) {
@@ -729,8 +721,10 @@ cudaError_t launch_pencil_fast(int axis, bool inv, const GridDev& g, const Penci
         case 144: return pencil_sized<144, 16, 16, 3, false>(axis, inv, g, j, st);
         case 256: return pencil_sized<256, 16, 16, 3, false>(axis, inv, g, j, st);
         case 480:
-            return pencil_double_buffer() ? pencil_sized<480, 32, 8, 2, true>(axis, inv, g, j, st)
-                                          : pencil_sized<480, 32, 8, 3, false>(axis, inv, g, j, st);
+            // measured on B200 (config D): prime-factor 32x15 is fastest for the x pass (no
+            // inter-level twiddles), Cooley-Tukey 30x16 for the y pass; both double-buffered
+            return axis == 0 ? pencil_sized<480, 32, 8, 2, true>(axis, inv, g, j, st)
+                             : pencil_sized<480, 30, 8, 2, true>(axis, inv, g, j, st);
         default: return cudaErrorInvalidValue;
     }
 }
