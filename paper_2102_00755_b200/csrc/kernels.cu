@@ -541,7 +541,7 @@ cudaError_t launch_zinv(const GridDev& g, const float2* S, const float2* premul,
 cudaError_t launch_adjoint_source(const float* sim, const double* obs, int nt, int ns, int integrate, float* q,
                                   double* loss_part, double* loss_out, double* loss_acc, int accumulate,
                                   cudaStream_t st) {
-    adjoint_source_kernel<<<(ns + 127) / 128, 128, 0, st>>>(sim, obs, nt, ns, integrate, q, loss_part);
+    if (ns > 0) adjoint_source_kernel<<<(ns + 127) / 128, 128, 0, st>>>(sim, obs, nt, ns, integrate, q, loss_part);
     loss_reduce_kernel<<<1, 32, 0, st>>>(loss_part, ns, loss_out, loss_acc, accumulate);
     return cudaGetLastError();
 }

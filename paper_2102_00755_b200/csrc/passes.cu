@@ -62,6 +62,8 @@ struct PencilCfg {
     static constexpr int CM = PFA ? (N1 * cx_inv_mod(N1 % N2, N2)) % L : 0;  // = 0 mod N1, 1 mod N2
     // tile buffer(s) (two with double-buffered prefetch) + transpose tile + twiddles
     static constexpr size_t SMEM = ((DB ? 2 : 1) * size_t(L) * TB + size_t(N1) * KP + L) * sizeof(float2);
+    // x pass: + kappa of the current tile (shared by the source groups of the tile)
+    static constexpr size_t SMEM_X = SMEM + size_t(L) * TB * sizeof(float);
     // row of input element (n1, n2) and of output element (k1, k2)
     __device__ __forceinline__ static int in_row(int n1, int n2) {
         if constexpr (PFA) {
@@ -99,6 +101,7 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
     float2* xbuf1 = DB ? smem + L * TB : smem;
     float2* ys = smem + (DB ? 2 : 1) * L * TB;  // transposed [N1][N2*TB (+pad)]
     float2* tw = ys + N1 * KP;                // W_L^k
+    float* kap_s = reinterpret_cast<float*>(tw + L);  // x pass: kappa of the current tile
     const FftPlan& plan = AXIS == 0 ? g.px : g.py;
     for (int i = threadIdx.x; i < L; i += NT) tw[i] = plan.tw[i];
 
@@ -228,13 +231,21 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
                 float2 X[N2];
                 forward(X);
                 if (inB) {
-                    const float ky = g.ky[w.line];
-                    const float kz = colok ? g.kz[w.c0 + c] : 0.f;
+                    if (kap && w.grp == 0) {
+                        // kappa(|k|) of this tile, evaluated once for all its source groups
+                        const float ky = g.ky[w.line];
+                        const float kz = colok ? g.kz[w.c0 + c] : 0.f;
+#pragma unroll
+                        for (int k2 = 0; k2 < N2; ++k2) {
+                            const int k = C::out_row(kb, k2);
+                            const float kx = g.kx[k];
+                            kap_s[k * TB + c] = kappa_fast(kx * kx + ky * ky + kz * kz, g.half_cdt);
+                        }
+                    }
 #pragma unroll
                     for (int k2 = 0; k2 < N2; ++k2) {
                         const int k = C::out_row(kb, k2);
-                        const float kx = g.kx[k];
-                        xs[k * TB + c] = kap ? cscale(X[k2], kappa_fast(kx * kx + ky * ky + kz * kz, g.half_cdt)) : X[k2];
+                        xs[k * TB + c] = kap ? cscale(X[k2], kap_s[k * TB + c]) : X[k2];
                     }
                 }
             }
@@ -685,13 +696,14 @@ cudaError_t run_pencil(const GridDev& g, const PencilJobs& j, cudaStream_t st) {
     using C = PencilCfg<L, N1, TB, DB>;
     auto kern = pencil_fast_kernel<AXIS, INV, L, N1, TB, MINB, DB>;
     static bool configured = false;
+    constexpr size_t smem = AXIS == 0 ? C::SMEM_X : C::SMEM;
     if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
     const int ntiles = ((g.nzh + TB - 1) / TB) * (AXIS == 0 ? g.ny : g.nx);
     const int grid = (!DB || ntiles < sm_count() * MINB) ? ntiles : sm_count() * MINB;
-    kern<<<grid, C::NT, C::SMEM, st>>>(g, j);
+    kern<<<grid, C::NT, smem, st>>>(g, j);
     return cudaGetLastError();
 }
 
