@@ -17,6 +17,7 @@ Arms:
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import statistics
@@ -38,7 +39,10 @@ BYTES_CORR_MODEL = 16.0      # per voxel per adjoint+TR pair-step
 def ncu_traffic(config_name: str, kernel_class: str):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, averaged over the
     launches of the class) from the committed ncu launch list of this config, if any."""
-    p = os.path.join(ROOT, "profiles", f"r1_launches_config{config_name}.json")
+    cands = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_launches_config{config_name}.json")))
+    if not cands:
+        return None, None
+    p = cands[-1]  # latest round
     try:
         d = json.load(open(p))
         return float(d["class_dram_bytes_per_launch_avg"][kernel_class]), os.path.relpath(p, ROOT)

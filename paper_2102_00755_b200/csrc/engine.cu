@@ -293,52 +293,71 @@ struct StepIO {
 
 // One leapfrog step of a stepper: update_velocity_density (engine.hpp:270-292), sparse
 // injection / shell enforcement, update_pressure (:318-347), gathers — 8 launches.
+// x-plane chunk of the y/z pass chains (0 = whole grid). With chunks, a chunk's
+// y-inverse -> z -> y-forward chain runs back to back so its spectra stay L2-resident.
+int chunk_planes(const Ctx& c) {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = std::getenv("USTFWI_CHUNK");
+        env = e ? std::max(0, std::atoi(e)) : 0;
+    }
+    if (use_generic_kernels() || !fast_rows_supported(c.g.nz)) return 0;
+    return env;
+}
+
 void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     const GridDev& g = c.g;
     const double SB = static_cast<double>(g.rows) * g.nzh * sizeof(float2);  // one half spectrum
     const double FB = static_cast<double>(g.N) * sizeof(float);               // one real field
-    auto pencil = [&](int axis, bool inv, const PencilJobs& j) {
+    const int ch = chunk_planes(c) > 0 ? std::min(chunk_planes(c), g.nx) : g.nx;
+    // run body(gc, frac) over the x-plane chunks
+    auto chunked = [&](auto&& body) {
+        for (int x0 = 0; x0 < g.nx; x0 += ch) {
+            GridDev gc = g;
+            gc.x0 = x0;
+            gc.xn = std::min(ch, g.nx - x0);
+            body(gc, static_cast<double>(gc.xn) / g.nx);
+        }
+    };
+    auto pencil = [&](const GridDev& gg, double frac, int axis, bool inv, const PencilJobs& j) {
         int loads = 0;
         for (int q = 0; q < j.n; ++q)
             if (q == 0 || j.job[q].src != j.job[q - 1].src) ++loads;
-        c.launch(axis == 0 ? KIND_X : KIND_Y, (loads + j.n) * SB, [&] { return launch_pencil(axis, inv, g, j, st); }, st);
+        c.launch(axis == 0 ? KIND_X : KIND_Y, frac * (loads + j.n) * SB,
+                 [&] { return launch_pencil(axis, inv, gg, j, st); }, st);
     };
     PencilJobs j{};
     for (int f = 0; f < 3; ++f) j.buf[f] = s.S[f];
-    // Y forward of Fz p
-    j.n = 1;
-    j.job[0] = {0, 0, nullptr, 0};
-    pencil(1, false, j);
+    // S0 holds Fy Fz p on entry (the previous step's pressure chain, or an initial state)
     // X: (kappa D_x+ , kappa)
     j.n = 2;
     j.job[0] = {0, 0, c.dmul[0][ST_PLUS], 1};
     j.job[1] = {0, 1, nullptr, 1};
-    pencil(0, false, j);
-    // Y inverse: S0 <- T_x, S2 <- T_kappa, S1 <- D_y+ T_kappa
-    j.n = 3;
-    j.job[0] = {0, 0, nullptr, 0};
-    j.job[1] = {1, 2, nullptr, 0};
-    j.job[2] = {1, 1, c.dmul[1][ST_PLUS], 0};
-    pencil(1, true, j);
-    // Z: c2r (D_z+ on S2), velocity update, r2c of v
+    pencil(g, 1.0, 0, false, j);
     Pml ps{{c.pml_stag[0], c.pml_stag[1], c.pml_stag[2]}};
     const double coef_b = c.dtr_stag[0].field ? 3 * FB : 0.0;
-    c.launch(KIND_ZVEL, 6 * SB + 6 * FB + coef_b,
-             [&] { return launch_zvel(g, s.S, c.dmul[2][ST_PLUS], s.v, ps, c.dtr_stag, st); }, st);
-    // Y forward x3
-    j.n = 3;
-    for (int f = 0; f < 3; ++f) j.job[f] = {f, f, nullptr, 0};
-    pencil(1, false, j);
+    chunked([&](const GridDev& gc, double frac) {
+        PencilJobs jj{};
+        for (int f = 0; f < 3; ++f) jj.buf[f] = s.S[f];
+        // Y inverse: S0 <- T_x, S2 <- T_kappa, S1 <- D_y+ T_kappa
+        jj.n = 3;
+        jj.job[0] = {0, 0, nullptr, 0};
+        jj.job[1] = {1, 2, nullptr, 0};
+        jj.job[2] = {1, 1, c.dmul[1][ST_PLUS], 0};
+        pencil(gc, frac, 1, true, jj);
+        // Z: c2r (D_z+ on S2), velocity update, r2c of v
+        c.launch(KIND_ZVEL, frac * (6 * SB + 6 * FB + coef_b),
+                 [&] { return launch_zvel(gc, s.S, c.dmul[2][ST_PLUS], s.v, ps, c.dtr_stag, st); }, st);
+        // Y forward x3
+        for (int f = 0; f < 3; ++f) jj.job[f] = {f, f, nullptr, 0};
+        pencil(gc, frac, 1, false, jj);
+    });
     // X: kappa D_x-, kappa, kappa
+    j.n = 3;
     j.job[0] = {0, 0, c.dmul[0][ST_MINUS], 1};
     j.job[1] = {1, 1, nullptr, 1};
     j.job[2] = {2, 2, nullptr, 1};
-    pencil(0, false, j);
-    // Y inverse x3 (D_y- on S1)
-    j.job[0] = {0, 0, nullptr, 0};
-    j.job[1] = {1, 1, c.dmul[1][ST_MINUS], 0};
-    j.job[2] = {2, 2, nullptr, 0};
-    pencil(1, true, j);
+    pencil(g, 1.0, 0, false, j);
     // Z: c2r (D_z- on S2), density update, sparse ops, pressure, gathers, Fz p
     ZrhoArgs a{};
     for (int f = 0; f < 3; ++f) {
@@ -364,8 +383,32 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     const bool split = !use_generic_kernels() && fast_rows_supported(g.nz);
     const double zb = 4 * SB + (split ? 11 : 8) * FB + (c.dtrho0.field ? FB : 0.0) + (io.corr.grad ? 5 * FB : 0.0);
     if (io.wait_before_z) CK(cudaStreamWaitEvent(st, io.wait_before_z, 0));
-    c.launch(KIND_ZRHO, zb, [&] { return launch_zrho(g, a, true, st); }, st);
-    if (split) ++c.launches;
+    chunked([&](const GridDev& gc, double frac) {
+        PencilJobs jj{};
+        for (int f = 0; f < 3; ++f) jj.buf[f] = s.S[f];
+        // Y inverse x3 (D_y- on S1)
+        jj.n = 3;
+        jj.job[0] = {0, 0, nullptr, 0};
+        jj.job[1] = {1, 1, c.dmul[1][ST_MINUS], 0};
+        jj.job[2] = {2, 2, nullptr, 0};
+        pencil(gc, frac, 1, true, jj);
+        c.launch(KIND_ZRHO, frac * zb, [&] { return launch_zrho(gc, a, true, st); }, st);
+        if (split) ++c.launches;
+        // Y forward of Fz p for the next step
+        jj.n = 1;
+        jj.job[0] = {0, 0, nullptr, 0};
+        pencil(gc, frac, 1, false, jj);
+    });
+}
+
+// Y forward of S0 (after a pressure refresh outside run_step): restores the run_step
+// entry invariant S0 = Fy Fz p.
+void y_forward_p(Ctx& c, Sim& s, cudaStream_t st) {
+    PencilJobs j{};
+    j.buf[0] = s.S[0];
+    j.n = 1;
+    j.job[0] = {0, 0, nullptr, 0};
+    c.count(launch_pencil(1, false, c.g, j, st));
 }
 
 // Build the device InjectSet for `n` contributions at flat positions pos[i].
@@ -539,6 +582,7 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
         a.enf = SparseEnforce{n_shell, c.shell_pos, shell_row(last), static_cast<float>(c.ndim)};
         a.diverged = c.flags;
         c.count(launch_zrho(c.g, a, false, sb));
+        y_forward_p(c, rep, sb);
     }
     // look-ahead step (gradient.hpp:438-441)
     StepIO rio;
@@ -662,6 +706,8 @@ int ustfwi_gpu_create(int device, const ustfwi_grid* grid, ustfwi_gpu_ctx** out)
         g.nzh = g.nz / 2 + 1;
         g.nzp = (g.nzh + 3) & ~3;
         g.rows = static_cast<long long>(g.nx) * g.ny;
+        g.x0 = 0;
+        g.xn = g.nx;
         g.N = g.rows * g.nz;
         if (g.N >= (1LL << 31)) fail(USTFWI_ERR_INVALID, "grid larger than 2^31 points is not supported");
         g.px = make_plan(*c, g.nx);

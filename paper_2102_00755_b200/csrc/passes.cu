@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
     gstart[ng] = jobs.n;
 
     const int ntx = (g.nzh + TB - 1) / TB;
-    const int ntiles = ntx * (AXIS == 0 ? g.ny : g.nx);
+    const int ntiles = ntx * (AXIS == 0 ? g.ny : g.xn);
+    const int line0 = AXIS == 0 ? 0 : g.x0;
     const int nunits = ((ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * ng;
     const int pitch = (AXIS == 0) ? g.ny * g.nzp : g.nzp;
     const int c = threadIdx.x % TB;
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
         Unit w;
         const int tile = (int)blockIdx.x + (u / ng) * (int)gridDim.x;
         w.grp = u % ng;
-        w.line = tile / ntx;
+        w.line = line0 + tile / ntx;
         w.c0 = (tile % ntx) * TB;
         w.ncol = min(TB, g.nzh - w.c0);
         w.base = (AXIS == 0) ? (long long)w.line * g.nzp + w.c0 : (long long)w.line * g.ny * g.nzp + w.c0;
@@ -400,8 +401,8 @@ __global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zvel_fast_kernel(const 
     float2* const Sa = A.S[a];
     float* const va = A.v[a];
 
-    const long long row0 = (long long)blockIdx.x * RW;
-    const int nrows = (int)min((long long)RW, g.rows - row0);
+    const long long row0 = (long long)g.x0 * g.ny + (long long)blockIdx.x * RW;
+    const int nrows = (int)min((long long)RW, (long long)(g.x0 + g.xn) * g.ny - row0);
     if (threadIdx.x == 0) mbar_init(bar, 1);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -478,8 +479,8 @@ __global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zrho_axis_kernel(const 
     const bool coef_field = A.dtrho0.field != nullptr;
     float* const ra = A.rho[a];
 
-    const long long row0 = (long long)blockIdx.x * RW;
-    const int nrows = (int)min((long long)RW, g.rows - row0);
+    const long long row0 = (long long)g.x0 * g.ny + (long long)blockIdx.x * RW;
+    const int nrows = (int)min((long long)RW, (long long)(g.x0 + g.xn) * g.ny - row0);
     const long long i0 = row0 * NZ;
     if (threadIdx.x == 0) mbar_init(bar, 1);
     __syncthreads();
@@ -541,8 +542,8 @@ __global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zp_kernel(const __grid_
     float2* zt = twM + M;
     float2* zn = zt + RW * C::ZT;
     __shared__ int sp[8];
-    const long long row0 = (long long)blockIdx.x * RW;
-    const int nrows = (int)min((long long)RW, g.rows - row0);
+    const long long row0 = (long long)g.x0 * g.ny + (long long)blockIdx.x * RW;
+    const int nrows = (int)min((long long)RW, (long long)(g.x0 + g.xn) * g.ny - row0);
     const long long i0 = row0 * NZ;
     const int lo_key = (int)i0;
     if (threadIdx.x == 0) {
@@ -701,7 +702,7 @@ cudaError_t run_pencil(const GridDev& g, const PencilJobs& j, cudaStream_t st) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    const int ntiles = ((g.nzh + TB - 1) / TB) * (AXIS == 0 ? g.ny : g.nx);
+    const int ntiles = ((g.nzh + TB - 1) / TB) * (AXIS == 0 ? g.ny : g.xn);
     const int grid = (!DB || ntiles < sm_count() * MINB) ? ntiles : sm_count() * MINB;
     kern<<<grid, C::NT, smem, st>>>(g, j);
     return cudaGetLastError();
@@ -767,7 +768,7 @@ cudaError_t zvel_sized(const GridDev& g, float2* S[3], const float2* dz_plus, fl
     const size_t smem = C::FIXED + size_t(kZRows) * g.nzp * 8 + size_t(r[0].field ? 2 : 1) * kZRows * C::NZ * 4;
     auto kern = zvel_fast_kernel<M, N1, kZRows>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const dim3 blocks((unsigned)((g.rows + kZRows - 1) / kZRows), 3);
+    const dim3 blocks((unsigned)(((long long)g.xn * g.ny + kZRows - 1) / kZRows), 3);
     kern<<<blocks, C::NT, smem, st>>>(a);
     return cudaGetLastError();
 }
@@ -777,7 +778,7 @@ cudaError_t zrho_sized(const GridDev& g, const ZrhoArgs& za, cudaStream_t st) {
     ZrhoFastArgs a;
     a.g = g;
     a.a = za;
-    const unsigned blocks = (unsigned)((g.rows + kZRows - 1) / kZRows);
+    const unsigned blocks = (unsigned)(((long long)g.xn * g.ny + kZRows - 1) / kZRows);
     // density update, one CTA per (row block, axis)
     const size_t smem1 = 16 + size_t(M) * 8 + size_t(kZRows) * C::ZT * 8 + size_t(kZRows) * g.nzp * 8 +
                          size_t(za.dtrho0.field ? 2 : 1) * kZRows * C::NZ * 4;
