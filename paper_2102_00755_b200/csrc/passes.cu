@@ -15,9 +15,13 @@
 // HBM read and one HBM write per output; kappa and the stagger factors are applied between
 // the halves. The z passes keep the elementwise velocity / density / pressure update,
 // sparse sources and shell, gathers and the c0 correlation in the same kernel.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <cstring>
+#include <vector>
 
 #include "async_copy.cuh"
 #include "fft_reg.cuh"
@@ -268,6 +272,198 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
         __syncthreads();  // xs / ys free for the next prefetch into this buffer and the next unit
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// TMA variant of the pencil pass: the [L][TB] tile of a unit arrives by TMA tensor loads
+// (one or two boxes, completion on an mbarrier per stage) and every output tile leaves by a
+// TMA tensor store from shared memory, so no thread computes a global address. One thread
+// of a warp that idles in phase A (the last thread) is the producer: it issues the loads /
+// stores and waits for the store reads before a staging buffer is reused.
+struct PencilMaps {
+    CUtensorMap tm[3];  // per scratch buffer, the box shape of this pass
+};
+
+template <int AXIS, bool INV, int L, int N1, int TB, int MINB, bool DB>
+__global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
+    pencil_tma_kernel(const __grid_constant__ GridDev g, const __grid_constant__ PencilJobs jobs,
+                      const __grid_constant__ PencilMaps maps) {
+    using C = PencilCfg<L, N1, TB, DB>;
+    constexpr int N2 = C::N2, KP = C::KP, NT = C::NT;
+    constexpr int NBUF = DB ? 2 : 1;
+    constexpr int BOXR = L > 256 ? L / 2 : L;  // TMA box extent <= 256 rows
+    constexpr int NBOX = L / BOXR;
+    constexpr unsigned TILE_BYTES = unsigned(L) * TB * sizeof(float2);
+    extern __shared__ __align__(128) unsigned char sm_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm_raw);          // one per stage
+    float2* xbuf = reinterpret_cast<float2*>(sm_raw + 128);       // [NBUF][L][TB], 128-B aligned
+    float2* ys = xbuf + NBUF * L * TB;                            // transposed [N1][KP]
+    float2* tw = ys + N1 * KP;                                    // W_L^k
+    float* kap_s = reinterpret_cast<float*>(tw + L);              // x pass: kappa of the tile
+    const FftPlan& plan = AXIS == 0 ? g.px : g.py;
+    const bool producer = threadIdx.x == NT - 1;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < NBUF; ++b) mbar_init(&bar[b], 1);
+    }
+    for (int i = threadIdx.x; i < L; i += NT) tw[i] = plan.tw[i];
+
+    int gstart[5];
+    int ng = 0;
+    for (int jb = 0; jb < jobs.n; ++jb)
+        if (jb == 0 || jobs.job[jb].src != jobs.job[jb - 1].src) gstart[ng++] = jb;
+    gstart[ng] = jobs.n;
+
+    const int ntx = (g.nzh + TB - 1) / TB;
+    const int ntiles = ntx * (AXIS == 0 ? g.ny : g.xn);
+    const int line0 = AXIS == 0 ? 0 : g.x0;
+    const int nunits = ((ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * ng;
+    const int c = threadIdx.x % TB;
+    const int ra = threadIdx.x / TB;
+    const bool inA = ra < N2, inB = ra < N1;
+    const int kb = C::out_base(ra);
+    __syncthreads();  // barriers initialised, twiddles staged
+
+    // tile coordinates of unit u: (float column, line, first row) in the 3-D tensor view
+    auto tile_of = [&](int u, int& line, int& col0, int& grp) {
+        const int tile = (int)blockIdx.x + (u / ng) * (int)gridDim.x;
+        grp = u % ng;
+        line = line0 + tile / ntx;
+        col0 = (tile % ntx) * TB;
+    };
+    auto box = [&](const CUtensorMap* tm, float2* s, int line, int col0, int q, bool load, uint64_t* b) {
+        const int r0 = q * BOXR;
+        const int e0 = 2 * col0;
+        const int e1 = AXIS == 0 ? line : r0;
+        const int e2 = AXIS == 0 ? r0 : line;
+        if (load) tma_load_3d(s + r0 * TB, tm, e0, e1, e2, b);
+        else tma_store_3d(tm, s + r0 * TB, e0, e1, e2);
+    };
+    auto prefetch = [&](int u) {
+        if (producer && u < nunits) {
+            int line, col0, grp;
+            tile_of(u, line, col0, grp);
+            const int b = u % NBUF;
+            float2* xs = xbuf + b * L * TB;
+            bulk_wait_read_all();  // the stage may still be the source of a store
+            mbar_arrive_expect_tx(&bar[b], TILE_BYTES);
+            const CUtensorMap* tm = &maps.tm[jobs.job[gstart[grp]].src];
+#pragma unroll
+            for (int q = 0; q < NBOX; ++q) box(tm, xs, line, col0, q, true, &bar[b]);
+        }
+    };
+    auto store_tile = [&](float2* xs, int dst, int line, int col0) {
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (producer) {
+#pragma unroll
+            for (int q = 0; q < NBOX; ++q) box(&maps.tm[dst], xs, line, col0, q, false, nullptr);
+            bulk_commit();
+        }
+    };
+
+    if (DB) prefetch(0);
+    for (int u = 0; u < nunits; ++u) {
+        const int b = u % NBUF;
+        float2* xs = xbuf + b * L * TB;
+        if (DB) prefetch(u + 1);
+        else prefetch(u);
+        mbar_wait(&bar[b], (u / NBUF) & 1);
+        int line, col0, grp;
+        tile_of(u, line, col0, grp);
+        const int gb = gstart[grp], ge = gstart[grp + 1];
+
+        // forward transform of xs -> X (phase-B registers); xs is free afterwards
+        auto forward = [&](float2 (&X)[N2]) {
+            if (inA) {
+                float2 a[N1];
+#pragma unroll
+                for (int n1 = 0; n1 < N1; ++n1) a[n1] = xs[C::in_row(n1, ra) * TB + c];
+                RDft<N1, false>::run(a);
+                if constexpr (!C::PFA) {
+#pragma unroll
+                    for (int k1 = 1; k1 < N1; ++k1) a[k1] = cmul(a[k1], tw[ra * k1]);
+                }
+#pragma unroll
+                for (int k1 = 0; k1 < N1; ++k1) ys[k1 * KP + ra * TB + c] = a[k1];
+            }
+            __syncthreads();
+            if (inB) {
+#pragma unroll
+                for (int n2 = 0; n2 < N2; ++n2) X[n2] = ys[ra * KP + n2 * TB + c];
+                RDft<N2, false>::run(X);
+            }
+        };
+        // inverse of b (phase-B registers, natural order), staged natural-order in xs, stored
+        auto inverse_store = [&](float2 (&bb)[N2], int dst) {
+            if (inB) {
+                RDft<N2, true>::run(bb);
+                if constexpr (!C::PFA) {
+#pragma unroll
+                    for (int n2 = 1; n2 < N2; ++n2) bb[n2] = cmul(bb[n2], conjf2(tw[ra * n2]));
+                }
+            }
+            if (producer) bulk_wait_read_all();  // previous store out of xs
+            __syncthreads();
+            if (inB) {
+#pragma unroll
+                for (int n2 = 0; n2 < N2; ++n2) ys[ra * KP + n2 * TB + c] = bb[n2];
+            }
+            __syncthreads();
+            if (inA) {
+                float2 a[N1];
+#pragma unroll
+                for (int k1 = 0; k1 < N1; ++k1) a[k1] = ys[k1 * KP + ra * TB + c];
+                RDft<N1, true>::run(a);
+#pragma unroll
+                for (int n1 = 0; n1 < N1; ++n1) xs[C::in_row(n1, ra) * TB + c] = a[n1];
+            }
+            store_tile(xs, dst, line, col0);
+        };
+
+        float2 X[N2];
+        if (AXIS == 1 && !INV) {
+            forward(X);
+            if (inB) {
+#pragma unroll
+                for (int k2 = 0; k2 < N2; ++k2) xs[C::out_row(kb, k2) * TB + c] = X[k2];
+            }
+            store_tile(xs, jobs.job[gb].dst, line, col0);
+        } else {
+            if (AXIS == 0) {
+                // forward x FFT then kappa (all jobs of a source share its kappa flag); kappa of
+                // the tile is evaluated once (first source group) into thread-private slots
+                forward(X);
+                if (inB && jobs.job[gb].kappa) {
+                    if (grp == 0) {
+                        const float ky = g.ky[line];
+                        const float kz = col0 + c < g.nzh ? g.kz[col0 + c] : 0.f;
+#pragma unroll
+                        for (int k2 = 0; k2 < N2; ++k2) {
+                            const int k = C::out_row(kb, k2);
+                            const float kx = g.kx[k];
+                            kap_s[k * TB + c] = kappa_fast(kx * kx + ky * ky + kz * kz, g.half_cdt);
+                        }
+                    }
+#pragma unroll
+                    for (int k2 = 0; k2 < N2; ++k2) X[k2] = cscale(X[k2], kap_s[C::out_row(kb, k2) * TB + c]);
+                }
+            } else if (inB) {
+#pragma unroll
+                for (int k2 = 0; k2 < N2; ++k2) X[k2] = xs[C::out_row(kb, k2) * TB + c];
+            }
+            for (int jb = gb; jb < ge; ++jb) {
+                const PencilJob J = jobs.job[jb];
+                float2 bb[N2];
+                if (inB) {
+#pragma unroll
+                    for (int k2 = 0; k2 < N2; ++k2)
+                        bb[k2] = J.dmul ? cmul(X[k2], __ldg(J.dmul + C::out_row(kb, k2))) : X[k2];
+                }
+                inverse_store(bb, J.dst);
+            }
+        }
+        __syncthreads();  // ys / kappa slots free for the next unit
+    }
+    if (producer) bulk_wait_all();
 }
 
 // ======================================================================================
@@ -708,8 +904,90 @@ cudaError_t run_pencil(const GridDev& g, const PencilJobs& j, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// ---- TMA tensor maps of the scratch spectra, viewed as fp32 [nx][ny][2*nzp] ----
+using EncodeTiledFn = PFN_cuTensorMapEncodeTiled_v12000;
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<EncodeTiledFn>(nullptr);
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+bool use_pencil_tma() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = std::getenv("USTFWI_PENCIL_TMA");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1 && encode_tiled() != nullptr;
+}
+
+// box = (2*TB floats, rows) along the pass axis; cached per thread (the map depends only on
+// the buffer address, the grid and the box, so a reused address gives the same map)
+bool pencil_map(CUtensorMap* out, const float2* buf, const GridDev& g, int axis, int TB, int boxr) {
+    struct Entry {
+        const float2* buf;
+        int nx, ny, nzp, axis, tb, boxr;
+        CUtensorMap map;
+    };
+    thread_local std::vector<Entry> cache;
+    for (const Entry& e : cache)
+        if (e.buf == buf && e.nx == g.nx && e.ny == g.ny && e.nzp == g.nzp && e.axis == axis && e.tb == TB &&
+            e.boxr == boxr) {
+            *out = e.map;
+            return true;
+        }
+    cuuint64_t dims[3] = {2ull * g.nzp, static_cast<cuuint64_t>(g.ny), static_cast<cuuint64_t>(g.nx)};
+    cuuint64_t strides[2] = {8ull * g.nzp, 8ull * g.nzp * g.ny};
+    cuuint32_t box[3] = {2u * TB, axis == 0 ? 1u : static_cast<cuuint32_t>(boxr),
+                         axis == 0 ? static_cast<cuuint32_t>(boxr) : 1u};
+    cuuint32_t es[3] = {1, 1, 1};
+    Entry e{buf, g.nx, g.ny, g.nzp, axis, TB, boxr, {}};
+    if (encode_tiled()(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(buf), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (cache.size() >= 64) cache.erase(cache.begin());
+    cache.push_back(e);
+    *out = e.map;
+    return true;
+}
+
+template <int AXIS, bool INV, int L, int N1, int TB, int MINB, bool DB>
+cudaError_t run_pencil_tma(const GridDev& g, const PencilJobs& j, cudaStream_t st) {
+    using C = PencilCfg<L, N1, TB, DB>;
+    constexpr int BOXR = L > 256 ? L / 2 : L;
+    PencilMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    for (int f = 0; f < 3; ++f)
+        if (j.buf[f] && !pencil_map(&maps.tm[f], j.buf[f], g, AXIS, TB, BOXR)) return cudaErrorInvalidValue;
+    auto kern = pencil_tma_kernel<AXIS, INV, L, N1, TB, MINB, DB>;
+    constexpr size_t smem = 128 + ((DB ? 2 : 1) * size_t(L) * TB + size_t(N1) * C::KP + L) * sizeof(float2) +
+                            (AXIS == 0 ? size_t(L) * TB * sizeof(float) : 0);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    const int ntiles = ((g.nzh + TB - 1) / TB) * (AXIS == 0 ? g.ny : g.xn);
+    const int grid = (!DB || ntiles < sm_count() * MINB) ? ntiles : sm_count() * MINB;
+    kern<<<grid, C::NT, smem, st>>>(g, j, maps);
+    return cudaGetLastError();
+}
+
 template <int L, int N1, int TB, int MINB, bool DB>
 cudaError_t pencil_sized(int axis, bool inv, const GridDev& g, const PencilJobs& j, cudaStream_t st) {
+    if (use_pencil_tma()) {
+        if (axis == 0) return run_pencil_tma<0, false, L, N1, TB, MINB, DB>(g, j, st);
+        return inv ? run_pencil_tma<1, true, L, N1, TB, MINB, DB>(g, j, st)
+                   : run_pencil_tma<1, false, L, N1, TB, MINB, DB>(g, j, st);
+    }
     if (axis == 0) return run_pencil<0, false, L, N1, TB, MINB, DB>(g, j, st);
     return inv ? run_pencil<1, true, L, N1, TB, MINB, DB>(g, j, st)
                : run_pencil<1, false, L, N1, TB, MINB, DB>(g, j, st);
