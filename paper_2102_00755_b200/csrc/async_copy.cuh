@@ -57,6 +57,12 @@ __device__ __forceinline__ void tma_store_3d(const void* tmap, const void* smem,
                  "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(smem))
                  : "memory");
 }
+// TMA bulk copy shared -> global (1-D), completion tracked by bulk groups
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gmem), "r"(smem_u32(smem)),
+                 "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 // the shared-memory sources of all committed bulk stores have been read
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }

@@ -873,6 +873,298 @@ __global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zp_kernel(const __grid_
 }
 
 // ======================================================================================
+// Row (z) passes, paired-residue layout. M = N1*N2 complex points per real row of 2M.
+// Thread t of a row owns the phase-B residues r0 = t and r1 = N1 - t (t = 0: 0 and N1/2), a
+// set closed under k -> M - k, so the real-FFT split/merge pairs X[k], X[M-k] are both in its
+// registers: every spectrum element is read from shared memory once. TPR = N1/2 threads per
+// row, all busy in both phases (phase A: N2/TPR codelets each). Rows are staged by TMA bulk
+// copies into padded, bank-conflict-free layouts and written back by TMA bulk stores.
+// ======================================================================================
+constexpr int pad_mod16(int x, int r) {
+    while (x % 16 != r) ++x;
+    return x;
+}
+
+template <int M, int N1>
+struct Z2 {
+    static constexpr int N2 = M / N1;
+    static constexpr int TPR = N1 / 2;
+    static constexpr int NA = N2 / TPR;
+    static constexpr int NZ = 2 * M;
+    static constexpr int ZP = N2 + 1;                     // zt: [k1][n2] per row
+    static constexpr int ZT = pad_mod16(N1 * ZP, TPR % 16);  // complex per zt row (rows of a warp on disjoint banks)
+    static constexpr int VP = 2 * pad_mod16(M, 4);        // floats per staged real row
+    static_assert(N1 % 2 == 0 && N2 % TPR == 0, "paired-residue split");
+};
+
+// W_{2M}^k as (W_{2M}^r) * (W_{2M}^{N1*k2}), the second factor compile-time
+template <int M, int N1, int K2>
+__device__ __forceinline__ float2 twr_of(float2 wr) {
+    return twmul<2 * M, N1 * K2, false>(wr);
+}
+
+// c2r phase B of one row: spectrum Xs (shared, >= M+1 bins) -> zt (shared), thread t.
+template <int M, int N1>
+__device__ __forceinline__ void z2_c2r_b(const float2* Xs, const float2* pre, const float2* twM, float2 wr0,
+                                         float2 wr1, int t, float2* zt) {
+    using C = Z2<M, N1>;
+    constexpr int N2 = C::N2, ZP = C::ZP;
+    const int r0 = t, r1 = t == 0 ? N1 / 2 : N1 - t;
+    float2 A[N2], B[N2];
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) {
+        A[k2] = Xs[r0 + N1 * k2];
+        B[k2] = Xs[r1 + N1 * k2];
+        if (pre) {
+            A[k2] = cmul(A[k2], pre[r0 + N1 * k2]);
+            B[k2] = cmul(B[k2], pre[r1 + N1 * k2]);
+        }
+    }
+    float2 XM = Xs[M];
+    if (pre) XM = cmul(XM, pre[M]);
+    if (t == 0) {  // DC and Nyquist bins: real parts only (fft.hpp:58-63 keeps the real output)
+        A[0].y = 0.f;
+        XM.y = 0.f;
+    }
+    auto zval = [](float2 a, float2 b, float2 w) {
+        const float2 e = make_float2(a.x + b.x, a.y - b.y);
+        const float2 d0 = make_float2(a.x - b.x, a.y + b.y);
+        const float2 o = make_float2(d0.x * w.x + d0.y * w.y, d0.y * w.x - d0.x * w.y);
+        return make_float2(e.x - o.y, e.y + o.x);
+    };
+    float2 za[N2], zb[N2];
+    static_for<0, N2>([&](auto K) {
+        constexpr int k2 = decltype(K)::value;
+        // partners of (r0, k2) and (r1, k2)
+        const float2 pa = t == 0 ? (k2 == 0 ? XM : A[(N2 - k2) % N2]) : B[N2 - 1 - k2];
+        const float2 pb = t == 0 ? B[N2 - 1 - k2] : A[N2 - 1 - k2];
+        za[k2] = zval(A[k2], pa, twr_of<M, N1, k2>(wr0));
+        zb[k2] = zval(B[k2], pb, twr_of<M, N1, k2>(wr1));
+    });
+    RDft<N2, true>::run(za);
+    RDft<N2, true>::run(zb);
+#pragma unroll
+    for (int n2 = 0; n2 < N2; ++n2) {
+        zt[r0 * ZP + n2] = n2 ? cmul(za[n2], conjf2(twM[r0 * n2])) : za[n2];
+        zt[r1 * ZP + n2] = n2 ? cmul(zb[n2], conjf2(twM[r1 * n2])) : zb[n2];
+    }
+}
+
+// c2r phase A: codelet j of thread t (n2 = t + TPR*j) -> scaled real pairs u[n1] of n = n2 + N2*n1
+template <int M, int N1>
+__device__ __forceinline__ void z2_c2r_a(const float2* zt, int n2, float scale, float2 (&u)[N1]) {
+    using C = Z2<M, N1>;
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) u[k1] = zt[k1 * C::ZP + n2];
+    RDft<N1, true>::run(u);
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) u[n1] = cscale(u[n1], scale);
+}
+
+// r2c phase A: pairs u[n1] of codelet n2 -> forward N1 codelet + twiddle -> zt
+template <int M, int N1>
+__device__ __forceinline__ void z2_r2c_a(float2 (&u)[N1], int n2, const float2* twM, float2* zt) {
+    using C = Z2<M, N1>;
+    RDft<N1, false>::run(u);
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) zt[k1 * C::ZP + n2] = k1 ? cmul(u[k1], twM[n2 * k1]) : u[k1];
+}
+
+// r2c phase B + split: zt -> half spectrum X[0..M] written to Xs (thread t's bins)
+template <int M, int N1>
+__device__ __forceinline__ void z2_r2c_b(const float2* zt, float2 wr0, float2 wr1, int t, float2* Xs) {
+    using C = Z2<M, N1>;
+    constexpr int N2 = C::N2, ZP = C::ZP;
+    const int r0 = t, r1 = t == 0 ? N1 / 2 : N1 - t;
+    float2 A[N2], B[N2];
+#pragma unroll
+    for (int n2 = 0; n2 < N2; ++n2) {
+        A[n2] = zt[r0 * ZP + n2];
+        B[n2] = zt[r1 * ZP + n2];
+    }
+    RDft<N2, false>::run(A);  // Z[r0 + N1*k2]
+    RDft<N2, false>::run(B);  // Z[r1 + N1*k2]
+    auto xval = [](float2 a, float2 b, float2 w) {
+        const float2 e = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y - b.y));
+        const float2 o = make_float2(0.5f * (a.y + b.y), -0.5f * (a.x - b.x));
+        return make_float2(e.x + (w.x * o.x - w.y * o.y), e.y + (w.x * o.y + w.y * o.x));
+    };
+    static_for<0, N2>([&](auto K) {
+        constexpr int k2 = decltype(K)::value;
+        const float2 pa = t == 0 ? A[(N2 - k2) % N2] : B[N2 - 1 - k2];
+        const float2 pb = t == 0 ? B[N2 - 1 - k2] : A[N2 - 1 - k2];
+        Xs[r0 + N1 * k2] = xval(A[k2], pa, twr_of<M, N1, k2>(wr0));
+        Xs[r1 + N1 * k2] = xval(B[k2], pb, twr_of<M, N1, k2>(wr1));
+    });
+    if (t == 0) Xs[M] = xval(A[0], A[0], make_float2(-1.f, 0.f));
+}
+
+// per-row staging: S rows (nzp complex, contiguous in HBM), real rows into a padded pitch
+template <int M, int N1, int RW>
+struct Z2Smem {
+    using C = Z2<M, N1>;
+    static constexpr size_t head = 128;  // mbarrier
+    static size_t bytes(int nzp, int nreal) {
+        return head + size_t(M) * 8 + size_t(M + 2) * 8 + size_t(RW) * nzp * 8 + size_t(RW) * C::ZT * 8 +
+               size_t(nreal) * RW * C::VP * 4;
+    }
+};
+
+// Velocity update, one CTA per (row block, axis) (engine.hpp:275-283):
+// c2r of kappa*D_a p (D_z+ on z), v_a = pml_a (pml_a v_a - dt/rho~_a * dp), r2c of v_a.
+template <int M, int N1, int RW>
+__global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zvel2_kernel(const __grid_constant__ ZvelFastArgs A) {
+    using C = Z2<M, N1>;
+    constexpr int N2 = C::N2, TPR = C::TPR, NA = C::NA, NZ = C::NZ, VP = C::VP, NT = RW * TPR;
+    extern __shared__ __align__(128) unsigned char sm_raw[];
+    const GridDev& g = A.g;
+    const int a = blockIdx.y;
+    const bool coef_field = A.r[a].field != nullptr;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm_raw);
+    float2* twM = reinterpret_cast<float2*>(sm_raw + 128);
+    float2* pre = twM + M;                       // D_z+ table (axis 2)
+    float2* sS = pre + (M + 2);  // keep 16-B alignment for the bulk copies                  // [RW][nzp]
+    float2* zt = sS + RW * g.nzp;                // [RW][ZT]
+    float* sV = reinterpret_cast<float*>(zt + RW * C::ZT);  // [RW][VP]
+    float* sR = sV + RW * VP;                    // [RW][VP] (coefficient field)
+    float2* const Sa = A.S[a];
+    float* const va = A.v[a];
+    const long long row0 = (long long)g.x0 * g.ny + (long long)blockIdx.x * RW;
+    const int nrows = (int)min((long long)RW, (long long)(g.x0 + g.xn) * g.ny - row0);
+
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_arrive_expect_tx(bar, nrows * g.nzp * 8u + (coef_field ? 2u : 1u) * nrows * NZ * 4u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        if (l == 0) bulk_g2s(sS, Sa + row0 * g.nzp, nrows * g.nzp * 8u, bar);
+        for (int i = l; i < nrows; i += 32) {
+            bulk_g2s(sV + i * VP, va + (row0 + i) * NZ, NZ * 4u, bar);
+            if (coef_field) bulk_g2s(sR + i * VP, A.r[a].field + (row0 + i) * NZ, NZ * 4u, bar);
+        }
+    }
+    for (int i = threadIdx.x; i < M; i += NT) twM[i] = g.pzh.tw[i];
+    if (a == 2)
+        for (int i = threadIdx.x; i <= M; i += NT) pre[i] = A.dz_plus[i];
+    const int r = threadIdx.x / TPR, t = threadIdx.x % TPR;
+    const bool rowok = r < nrows;
+    const long long row = row0 + r;
+    const int x = rowok ? (int)(row / g.ny) : 0, y = rowok ? (int)(row % g.ny) : 0;
+    const float2 wr0 = g.tw_rfft[t], wr1 = g.tw_rfft[t == 0 ? N1 / 2 : N1 - t];
+    float2* ztr = zt + r * C::ZT;
+    __syncthreads();
+    mbar_wait(bar, 0);
+
+    if (rowok) z2_c2r_b<M, N1>(sS + r * g.nzp, a == 2 ? pre : nullptr, twM, wr0, wr1, t, ztr);
+    __syncthreads();
+    if (rowok) {
+        const float pa = a == 0 ? __ldg(A.pml.prof[0] + x) : (a == 1 ? __ldg(A.pml.prof[1] + y) : 0.f);
+        const float rsc = A.r[a].scalar;
+        float* vs = sV + r * VP;
+        const float* rs = sR + r * VP;
+#pragma unroll
+        for (int j = 0; j < NA; ++j) {
+            const int n2 = t + TPR * j;
+            float2 u[N1];
+            z2_c2r_a<M, N1>(ztr, n2, g.inv_n, u);
+#pragma unroll
+            for (int n1 = 0; n1 < N1; ++n1) {
+                const int n = n2 + N2 * n1;
+                float2 vv = *reinterpret_cast<const float2*>(vs + 2 * n);
+                float2 pm = make_float2(pa, pa);
+                if (a == 2) pm = __ldg(reinterpret_cast<const float2*>(A.pml.prof[2]) + n);
+                float2 rr = make_float2(rsc, rsc);
+                if (coef_field) rr = *reinterpret_cast<const float2*>(rs + 2 * n);
+                vv.x = pm.x * (pm.x * vv.x - rr.x * u[n1].x);
+                vv.y = pm.y * (pm.y * vv.y - rr.y * u[n1].y);
+                *reinterpret_cast<float2*>(va + row * NZ + 2 * n) = vv;
+                u[n1] = vv;
+            }
+            z2_r2c_a<M, N1>(u, n2, twM, ztr);  // the same zt entries this thread just read
+        }
+    }
+    __syncthreads();
+    if (rowok) z2_r2c_b<M, N1>(ztr, wr0, wr1, t, Sa + row * g.nzp);
+}
+
+// Density update of one axis per CTA (engine.hpp:284-291): c2r of dv_a/dx_a (D_z- on z),
+// rho_a = pml_a (pml_a rho_a - dt rho0 dv_a).
+template <int M, int N1, int RW>
+__global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const __grid_constant__ ZrhoFastArgs P) {
+    using C = Z2<M, N1>;
+    constexpr int N2 = C::N2, TPR = C::TPR, NA = C::NA, NZ = C::NZ, VP = C::VP, NT = RW * TPR;
+    extern __shared__ __align__(128) unsigned char sm_raw[];
+    const GridDev& g = P.g;
+    const ZrhoArgs& A = P.a;
+    const int a = blockIdx.y;
+    const bool coef_field = A.dtrho0.field != nullptr;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm_raw);
+    float2* twM = reinterpret_cast<float2*>(sm_raw + 128);
+    float2* pre = twM + M;
+    float2* sS = pre + (M + 2);  // keep 16-B alignment for the bulk copies
+    float2* zt = sS + RW * g.nzp;
+    float* sR = reinterpret_cast<float*>(zt + RW * C::ZT);  // rho_a rows
+    float* sD = sR + RW * VP;                               // dt*rho0 field rows (optional)
+    float* const ra = A.rho[a];
+    const long long row0 = (long long)g.x0 * g.ny + (long long)blockIdx.x * RW;
+    const int nrows = (int)min((long long)RW, (long long)(g.x0 + g.xn) * g.ny - row0);
+
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_arrive_expect_tx(bar, nrows * g.nzp * 8u + (coef_field ? 2u : 1u) * nrows * NZ * 4u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        if (l == 0) bulk_g2s(sS, A.S[a] + row0 * g.nzp, nrows * g.nzp * 8u, bar);
+        for (int i = l; i < nrows; i += 32) {
+            bulk_g2s(sR + i * VP, ra + (row0 + i) * NZ, NZ * 4u, bar);
+            if (coef_field) bulk_g2s(sD + i * VP, A.dtrho0.field + (row0 + i) * NZ, NZ * 4u, bar);
+        }
+    }
+    for (int i = threadIdx.x; i < M; i += NT) twM[i] = g.pzh.tw[i];
+    if (a == 2)
+        for (int i = threadIdx.x; i <= M; i += NT) pre[i] = A.dz_minus[i];
+    const int r = threadIdx.x / TPR, t = threadIdx.x % TPR;
+    const bool rowok = r < nrows;
+    const long long row = row0 + r;
+    const int x = rowok ? (int)(row / g.ny) : 0, y = rowok ? (int)(row % g.ny) : 0;
+    const float2 wr0 = g.tw_rfft[t], wr1 = g.tw_rfft[t == 0 ? N1 / 2 : N1 - t];
+    float2* ztr = zt + r * C::ZT;
+    __syncthreads();
+    mbar_wait(bar, 0);
+
+    if (rowok) z2_c2r_b<M, N1>(sS + r * g.nzp, a == 2 ? pre : nullptr, twM, wr0, wr1, t, ztr);
+    __syncthreads();
+    if (rowok) {
+        const float pa = a == 0 ? __ldg(A.pml.prof[0] + x) : (a == 1 ? __ldg(A.pml.prof[1] + y) : 0.f);
+        const float dsc = A.dtrho0.scalar;
+        float* rs = sR + r * VP;
+        const float* ds = sD + r * VP;
+#pragma unroll
+        for (int j = 0; j < NA; ++j) {
+            const int n2 = t + TPR * j;
+            float2 u[N1];
+            z2_c2r_a<M, N1>(ztr, n2, g.inv_n, u);
+#pragma unroll
+            for (int n1 = 0; n1 < N1; ++n1) {
+                const int n = n2 + N2 * n1;
+                float2 q = *reinterpret_cast<const float2*>(rs + 2 * n);
+                float2 pm = make_float2(pa, pa);
+                if (a == 2) pm = __ldg(reinterpret_cast<const float2*>(A.pml.prof[2]) + n);
+                float2 d = make_float2(dsc, dsc);
+                if (coef_field) d = *reinterpret_cast<const float2*>(ds + 2 * n);
+                q.x = pm.x * (pm.x * q.x - d.x * u[n1].x);
+                q.y = pm.y * (pm.y * q.y - d.y * u[n1].y);
+                *reinterpret_cast<float2*>(ra + row * NZ + 2 * n) = q;
+            }
+        }
+    }
+}
+
+// ======================================================================================
 // dispatch
 // ======================================================================================
 namespace {
@@ -1030,6 +1322,50 @@ bool fast_rows_supported(int nz) {
 namespace {
 constexpr int kZRows = 8;
 
+bool use_zrow2() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = std::getenv("USTFWI_ZROW2");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+template <int M, int N1, int RW>
+cudaError_t zvel2_run(const GridDev& g, const ZvelFastArgs& a, cudaStream_t st) {
+    const size_t smem = Z2Smem<M, N1, RW>::bytes(g.nzp, a.r[0].field ? 2 : 1);
+    auto kern = zvel2_kernel<M, N1, RW>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const dim3 blocks((unsigned)(((long long)g.xn * g.ny + RW - 1) / RW), 3);
+    kern<<<blocks, RW * Z2<M, N1>::TPR, smem, st>>>(a);
+    return cudaGetLastError();
+}
+template <int M, int N1, int RW>
+cudaError_t zrho2_run(const GridDev& g, const ZrhoFastArgs& a, cudaStream_t st) {
+    const size_t smem = Z2Smem<M, N1, RW>::bytes(g.nzp, a.a.dtrho0.field ? 2 : 1);
+    auto kern = zrho2_axis_kernel<M, N1, RW>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const dim3 blocks((unsigned)(((long long)g.xn * g.ny + RW - 1) / RW), 3);
+    kern<<<blocks, RW * Z2<M, N1>::TPR, smem, st>>>(a);
+    return cudaGetLastError();
+}
+template <int M>
+cudaError_t zvel2_sized(const GridDev& g, const ZvelFastArgs& a, cudaStream_t st) {
+    if constexpr (M == 128) return zvel2_run<128, 16, 16>(g, a, st);
+    else if constexpr (M == 64) return zvel2_run<64, 8, 16>(g, a, st);
+    else if constexpr (M == 72) return zvel2_run<72, 6, 32>(g, a, st);
+    else if constexpr (M == 48) return zvel2_run<48, 4, 32>(g, a, st);
+    else return zvel2_run<32, 4, 32>(g, a, st);
+}
+template <int M>
+cudaError_t zrho2_sized(const GridDev& g, const ZrhoFastArgs& a, cudaStream_t st) {
+    if constexpr (M == 128) return zrho2_run<128, 16, 16>(g, a, st);
+    else if constexpr (M == 64) return zrho2_run<64, 8, 16>(g, a, st);
+    else if constexpr (M == 72) return zrho2_run<72, 6, 32>(g, a, st);
+    else if constexpr (M == 48) return zrho2_run<48, 4, 32>(g, a, st);
+    else return zrho2_run<32, 4, 32>(g, a, st);
+}
+
 template <int M, int N1>
 cudaError_t zvel_sized(const GridDev& g, float2* S[3], const float2* dz_plus, float* v[3], const Pml& pml,
                        const Coef r[3], cudaStream_t st) {
@@ -1043,6 +1379,7 @@ cudaError_t zvel_sized(const GridDev& g, float2* S[3], const float2* dz_plus, fl
     }
     a.dz_plus = dz_plus;
     a.pml = pml;
+    if (use_zrow2()) return zvel2_sized<M>(g, a, st);
     const size_t smem = C::FIXED + size_t(kZRows) * g.nzp * 8 + size_t(r[0].field ? 2 : 1) * kZRows * C::NZ * 4;
     auto kern = zvel_fast_kernel<M, N1, kZRows>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1058,6 +1395,10 @@ cudaError_t zrho_sized(const GridDev& g, const ZrhoArgs& za, cudaStream_t st) {
     a.a = za;
     const unsigned blocks = (unsigned)(((long long)g.xn * g.ny + kZRows - 1) / kZRows);
     // density update, one CTA per (row block, axis)
+    if (use_zrow2()) {
+        cudaError_t e = zrho2_sized<M>(g, a, st);
+        if (e != cudaSuccess) return e;
+    } else {
     const size_t smem1 = 16 + size_t(M) * 8 + size_t(kZRows) * C::ZT * 8 + size_t(kZRows) * g.nzp * 8 +
                          size_t(za.dtrho0.field ? 2 : 1) * kZRows * C::NZ * 4;
     auto k1 = zrho_axis_kernel<M, N1, kZRows>;
@@ -1065,6 +1406,7 @@ cudaError_t zrho_sized(const GridDev& g, const ZrhoArgs& za, cudaStream_t st) {
     k1<<<dim3(blocks, 3), C::NT, smem1, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    }
     // pressure, sparse work, gathers, correlation, r2c of p
     const size_t smem2 = C::FIXED;
     auto k2 = zp_kernel<M, N1, kZRows>;
