@@ -1164,6 +1164,140 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const _
     }
 }
 
+// Pressure step in the paired-residue layout (update_pressure, engine.hpp:318-326), with the
+// sparse work between the density update and p (mass sources :296-300, shell Dirichlet
+// :304-307), the gathers (simulate.hpp:88-95), the TR correlation (gradient.hpp:177-182)
+// and the r2c of p. Sparse updates are applied by the owner thread of each position straight
+// to the split densities in HBM, in reference order, before that thread reads them.
+template <int M, int N1, int RW>
+__global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zp2_kernel(const __grid_constant__ ZrhoFastArgs P) {
+    using C = Z2<M, N1>;
+    constexpr int N2 = C::N2, TPR = C::TPR, NA = C::NA, NZ = C::NZ, NT = RW * TPR;
+    extern __shared__ __align__(128) unsigned char sm_raw[];
+    const GridDev& g = P.g;
+    const ZrhoArgs& A = P.a;
+    float2* twM = reinterpret_cast<float2*>(sm_raw);
+    float2* zt = twM + M;
+    __shared__ int sp[8];
+    const long long row0 = (long long)g.x0 * g.ny + (long long)blockIdx.x * RW;
+    const int nrows = (int)min((long long)RW, (long long)(g.x0 + g.xn) * g.ny - row0);
+    const long long i0 = row0 * NZ;
+    const int lo_key = (int)i0;
+    if (threadIdx.x == 0) {
+        const int hi_key = (int)(i0 + (long long)nrows * NZ);
+        auto lb = [](const int* a, int n, int key) {
+            int lo = 0, hi = n;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (a[mid] < key) lo = mid + 1;
+                else hi = mid;
+            }
+            return lo;
+        };
+        sp[0] = A.inj.n_unique ? lb(A.inj.pos, A.inj.n_unique, lo_key) : 0;
+        sp[1] = A.inj.n_unique ? lb(A.inj.pos, A.inj.n_unique, hi_key) : 0;
+        sp[2] = A.enf.n ? lb(A.enf.pos, A.enf.n, lo_key) : 0;
+        sp[3] = A.enf.n ? lb(A.enf.pos, A.enf.n, hi_key) : 0;
+        sp[4] = A.sens.n ? lb(A.sens.pos, A.sens.n, lo_key) : 0;
+        sp[5] = A.sens.n ? lb(A.sens.pos, A.sens.n, hi_key) : 0;
+        sp[6] = A.shell.n ? lb(A.shell.pos, A.shell.n, lo_key) : 0;
+        sp[7] = A.shell.n ? lb(A.shell.pos, A.shell.n, hi_key) : 0;
+    }
+    for (int i = threadIdx.x; i < M; i += NT) twM[i] = g.pzh.tw[i];
+    const int r = threadIdx.x / TPR, t = threadIdx.x % TPR;
+    const bool rowok = r < nrows;
+    const long long row = row0 + r;
+    float2* ztr = zt + r * C::ZT;
+    __syncthreads();  // sp[] and twiddles ready
+
+    // owner of flat position pos: row, pair n = z/2 with n % N2 in this thread's codelets
+    auto owns = [&](int pos, int& j, int& n1, int& comp) {
+        const int tt = pos - lo_key;
+        const int rr = tt / NZ, z = tt % NZ, n = z >> 1;
+        comp = z & 1;
+        const int n2 = n % N2;
+        if (!(rowok && rr == r && n2 % TPR == t)) return false;
+        j = n2 / TPR;
+        n1 = n / N2;
+        return true;
+    };
+    // sparse density updates, in the reference order (sources, then the shell)
+    if (rowok) {
+        for (int u = sp[0]; u < sp[1]; ++u) {
+            const int pos = A.inj.pos[u];
+            int j, n1, comp;
+            if (!owns(pos, j, n1, comp)) continue;
+            const float sc = A.inj.scale[u];
+            for (int cc = A.inj.csr[u]; cc < A.inj.csr[u + 1]; ++cc) {
+                const int n = A.step_n - A.inj.delay[cc];
+                if (n < 0 || n >= A.inj.len[cc]) continue;
+                const float amp = A.inj.w[cc] * A.inj.sig[A.inj.off[cc] + (long long)n * A.inj.stride[cc]];
+                if (amp == 0.f) continue;
+                for (int aa = max(A.a_first, 0); aa < 3; ++aa) A.rho[aa][pos] += amp * sc;
+            }
+        }
+        for (int q = sp[2]; q < sp[3]; ++q) {
+            const int pos = A.enf.pos[q];
+            int j, n1, comp;
+            if (!owns(pos, j, n1, comp)) continue;
+            const float v = A.enf.vals[q] / (A.enf.ndim * A.c0sq[pos]);
+            for (int aa = max(A.a_first, 0); aa < 3; ++aa) A.rho[aa][pos] = v;
+        }
+    }
+
+    float2 pv[NA][N1];
+    if (rowok) {
+#pragma unroll
+        for (int j = 0; j < NA; ++j) {
+            const int n2 = t + TPR * j;
+#pragma unroll
+            for (int n1 = 0; n1 < N1; ++n1) {
+                const long long i = row * NZ + 2 * (n2 + N2 * n1);
+                const float2 q0 = *reinterpret_cast<const float2*>(A.rho[0] + i);
+                const float2 q1 = *reinterpret_cast<const float2*>(A.rho[1] + i);
+                const float2 q2 = *reinterpret_cast<const float2*>(A.rho[2] + i);
+                const float2 c2 = __ldg(reinterpret_cast<const float2*>(A.c0sq + i));
+                float2 p;
+                p.x = c2.x * ((q0.x + q1.x) + q2.x);
+                p.y = c2.y * ((q0.y + q1.y) + q2.y);
+                *reinterpret_cast<float2*>(A.p_out + i) = p;
+                pv[j][n1] = p;
+                if (A.corr.grad != nullptr) {
+                    const float2 pm = *reinterpret_cast<const float2*>(A.corr.p_mid + i);
+                    const float2 po = *reinterpret_cast<const float2*>(A.corr.p_old + i);
+                    const float2 qa = *reinterpret_cast<const float2*>(A.corr.q_adj + i);
+                    float2 gv = *reinterpret_cast<const float2*>(A.corr.grad + i);
+                    const float wx = 2.f / (c2.x * sqrtf(c2.x)), wy = 2.f / (c2.y * sqrtf(c2.y));
+                    gv.x += wx * (((p.x - 2.f * pm.x) + po.x) * A.corr.inv_dt) * qa.x;
+                    gv.y += wy * (((p.y - 2.f * pm.y) + po.y) * A.corr.inv_dt) * qa.y;
+                    *reinterpret_cast<float2*>(A.corr.grad + i) = gv;
+                }
+            }
+        }
+        if (A.check_step > 0 && row == 0 && t == 0 && !isfinite(pv[0][0].x)) atomicMin(A.diverged, A.check_step);
+        // gathers of p by the owner thread
+        auto gather = [&](int pos, float* out) {
+            int j, n1, comp;
+            if (!owns(pos, j, n1, comp)) return;
+#pragma unroll
+            for (int jj = 0; jj < NA; ++jj)
+#pragma unroll
+                for (int k = 0; k < N1; ++k)
+                    if (jj == j && k == n1) *out = comp ? pv[jj][k].y : pv[jj][k].x;
+        };
+        for (int s = sp[4]; s < sp[5]; ++s) gather(A.sens.pos[s], A.sens.out + A.sens.idx[s]);
+        for (int q = sp[6]; q < sp[7]; ++q) gather(A.shell.pos[q], A.shell.out + q);
+        // forward r2c of p into S0
+#pragma unroll
+        for (int j = 0; j < NA; ++j) z2_r2c_a<M, N1>(pv[j], t + TPR * j, twM, ztr);
+    }
+    __syncthreads();
+    if (rowok) {
+        const float2 wr0 = g.tw_rfft[t], wr1 = g.tw_rfft[t == 0 ? N1 / 2 : N1 - t];
+        z2_r2c_b<M, N1>(ztr, wr0, wr1, t, A.S[0] + row * g.nzp);
+    }
+}
+
 // ======================================================================================
 // dispatch
 // ======================================================================================
@@ -1347,6 +1481,12 @@ cudaError_t zrho2_run(const GridDev& g, const ZrhoFastArgs& a, cudaStream_t st) 
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const dim3 blocks((unsigned)(((long long)g.xn * g.ny + RW - 1) / RW), 3);
     kern<<<blocks, RW * Z2<M, N1>::TPR, smem, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    auto kp = zp2_kernel<M, N1, RW>;
+    const size_t smem_p = (size_t(M) + size_t(RW) * Z2<M, N1>::ZT) * sizeof(float2);
+    cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
+    kp<<<blocks.x, RW * Z2<M, N1>::TPR, smem_p, st>>>(a);
     return cudaGetLastError();
 }
 template <int M>
@@ -1395,10 +1535,8 @@ cudaError_t zrho_sized(const GridDev& g, const ZrhoArgs& za, cudaStream_t st) {
     a.a = za;
     const unsigned blocks = (unsigned)(((long long)g.xn * g.ny + kZRows - 1) / kZRows);
     // density update, one CTA per (row block, axis)
-    if (use_zrow2()) {
-        cudaError_t e = zrho2_sized<M>(g, a, st);
-        if (e != cudaSuccess) return e;
-    } else {
+    if (use_zrow2()) return zrho2_sized<M>(g, a, st);
+    {
     const size_t smem1 = 16 + size_t(M) * 8 + size_t(kZRows) * C::ZT * 8 + size_t(kZRows) * g.nzp * 8 +
                          size_t(za.dtrho0.field ? 2 : 1) * kZRows * C::NZ * 4;
     auto k1 = zrho_axis_kernel<M, N1, kZRows>;
