@@ -1247,30 +1247,44 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zp2_kernel(const __grid_c
 
     float2 pv[NA][N1];
     if (rowok) {
+        // loads of a chunk of pairs are issued before any store of the chunk (the output
+        // pointers may alias the inputs as far as the compiler knows)
+        constexpr int CH = N1 % 4 == 0 ? 4 : (N1 % 2 == 0 ? 2 : 1);
+        const bool corr = A.corr.grad != nullptr;
 #pragma unroll
         for (int j = 0; j < NA; ++j) {
             const int n2 = t + TPR * j;
 #pragma unroll
-            for (int n1 = 0; n1 < N1; ++n1) {
-                const long long i = row * NZ + 2 * (n2 + N2 * n1);
-                const float2 q0 = *reinterpret_cast<const float2*>(A.rho[0] + i);
-                const float2 q1 = *reinterpret_cast<const float2*>(A.rho[1] + i);
-                const float2 q2 = *reinterpret_cast<const float2*>(A.rho[2] + i);
-                const float2 c2 = __ldg(reinterpret_cast<const float2*>(A.c0sq + i));
-                float2 p;
-                p.x = c2.x * ((q0.x + q1.x) + q2.x);
-                p.y = c2.y * ((q0.y + q1.y) + q2.y);
-                *reinterpret_cast<float2*>(A.p_out + i) = p;
-                pv[j][n1] = p;
-                if (A.corr.grad != nullptr) {
-                    const float2 pm = *reinterpret_cast<const float2*>(A.corr.p_mid + i);
-                    const float2 po = *reinterpret_cast<const float2*>(A.corr.p_old + i);
-                    const float2 qa = *reinterpret_cast<const float2*>(A.corr.q_adj + i);
-                    float2 gv = *reinterpret_cast<const float2*>(A.corr.grad + i);
-                    const float wx = 2.f / (c2.x * sqrtf(c2.x)), wy = 2.f / (c2.y * sqrtf(c2.y));
-                    gv.x += wx * (((p.x - 2.f * pm.x) + po.x) * A.corr.inv_dt) * qa.x;
-                    gv.y += wy * (((p.y - 2.f * pm.y) + po.y) * A.corr.inv_dt) * qa.y;
-                    *reinterpret_cast<float2*>(A.corr.grad + i) = gv;
+            for (int h = 0; h < N1; h += CH) {
+                float2 q0[CH], q1[CH], q2[CH], c2[CH], pm[CH], po[CH], qa[CH], gv[CH];
+#pragma unroll
+                for (int e = 0; e < CH; ++e) {
+                    const long long i = row * NZ + 2 * (n2 + N2 * (h + e));
+                    q0[e] = *reinterpret_cast<const float2*>(A.rho[0] + i);
+                    q1[e] = *reinterpret_cast<const float2*>(A.rho[1] + i);
+                    q2[e] = *reinterpret_cast<const float2*>(A.rho[2] + i);
+                    c2[e] = __ldg(reinterpret_cast<const float2*>(A.c0sq + i));
+                    if (corr) {
+                        pm[e] = __ldg(reinterpret_cast<const float2*>(A.corr.p_mid + i));
+                        po[e] = __ldg(reinterpret_cast<const float2*>(A.corr.p_old + i));
+                        qa[e] = __ldg(reinterpret_cast<const float2*>(A.corr.q_adj + i));
+                        gv[e] = *reinterpret_cast<const float2*>(A.corr.grad + i);
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < CH; ++e) {
+                    const long long i = row * NZ + 2 * (n2 + N2 * (h + e));
+                    float2 p;
+                    p.x = c2[e].x * ((q0[e].x + q1[e].x) + q2[e].x);
+                    p.y = c2[e].y * ((q0[e].y + q1[e].y) + q2[e].y);
+                    *reinterpret_cast<float2*>(A.p_out + i) = p;
+                    pv[j][h + e] = p;
+                    if (corr) {
+                        const float wx = 2.f / (c2[e].x * sqrtf(c2[e].x)), wy = 2.f / (c2[e].y * sqrtf(c2[e].y));
+                        gv[e].x += wx * (((p.x - 2.f * pm[e].x) + po[e].x) * A.corr.inv_dt) * qa[e].x;
+                        gv[e].y += wy * (((p.y - 2.f * pm[e].y) + po[e].y) * A.corr.inv_dt) * qa[e].y;
+                        *reinterpret_cast<float2*>(A.corr.grad + i) = gv[e];
+                    }
                 }
             }
         }

@@ -11,6 +11,6 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     > gpurun_out/ncu_list_$tag.log 2>&1
 echo "ncu list rc=$?"
 python scripts/prof_step.py --config D --nt 4 --grad > gpurun_out/prof_plain_$tag.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"pencil_fast|zvel_fast|zrho_axis|zp_kernel" -s 0 -c 9 \
+ncu --set full --clock-control none --import-source on -k regex:"pencil_|zvel|zrho|zp_kernel|zp2_kernel" -s 0 -c 9 \
     -o gpurun_out/prof_full_$tag python scripts/prof_step.py --config D --nt 4 --grad > gpurun_out/ncu_full_$tag.log 2>&1
 echo "ncu full rc=$?"

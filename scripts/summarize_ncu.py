@@ -15,12 +15,12 @@ import sys
 
 
 def kclass(name):
-    m = re.search(r"pencil_fast_kernel<(\d)", name)
+    m = re.search(r"pencil_(?:fast|tma)_kernel<(\d)", name)
     if m:
         return "x_pass" if m.group(1) == "0" else "y_pass"
     if "zvel" in name:
         return "z_vel"
-    if "zrho" in name or "zp_kernel" in name:
+    if "zrho" in name or "zp_kernel" in name or "zp2_kernel" in name:
         return "z_rho"
     if "pencil" in name:
         return "y_pass"
@@ -59,7 +59,7 @@ def launches(path, out, cmd):
         s["us"] += d.get("us", 0)
         s["bytes"] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
         # bench counts one z_rho launch per (zrho_axis, zp) pair
-        if c != "z_rho" or "zp_kernel" in d["name"]:
+        if c != "z_rho" or "zp_kernel" in d["name"] or "zp2_kernel" in d["name"]:
             s["launches"] += 1
     res = {
         "command": " ".join(cmd),
