@@ -106,8 +106,9 @@ USTFWI_API void ustfwi_gpu_destroy(ustfwi_gpu_ctx* ctx);
 
 /* Medium (solver/medium.hpp:26-58) + the per-medium part of the WaveStepper constructor
  * (engine.hpp:184-259): CFL guard (NumericalError), c0^2, dt*rho0, dt/rho0 staggered via
- * fourier_shift. alpha0 may be NULL (lossless); gamma may be NULL. Absorbing media
- * (alpha0 != 0) are rejected with USTFWI_ERR_INVALID in this version. */
+ * fourier_shift. alpha0 may be NULL (lossless); gamma may be NULL. alpha0 != 0 enables the
+ * power-law absorption of update_pressure (engine.hpp:233-246,327-343; dispersion term
+ * unless y == 2) and the absorption terms of the c0 gradient (gradient.hpp:63-74,183-203). */
 USTFWI_API int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* ctx, const double* c0, const double* rho0,
                           const double* alpha0, double y, const uint8_t* gamma, double c0_min,
                           double c0_max);

@@ -129,6 +129,26 @@ struct ustfwi_gpu_ctx {
     std::vector<double> c0_host;
 
     Sim sim[2];
+    // absorbing media (engine.hpp:233-246; gradient.hpp:63-74): coefficient fields and
+    // per-stepper scratch, allocated only when alpha0 != 0
+    bool absorbing = false;
+    bool dispersion = false;
+    double y_pow = 1.5;
+    float* abs_coef = nullptr;     // tau0, eta, wa1, wa2 (4 fields)
+    float* tau0 = nullptr;
+    float* eta = nullptr;
+    float* wa1 = nullptr;
+    float* wa2 = nullptr;
+    struct AbsScratch {
+        float* du[3] = {};
+        float* ain = nullptr;
+        float* aout = nullptr;
+        float* aout2 = nullptr;
+        float* sum = nullptr;
+    } abs_s[2];
+    float* abs_mem = nullptr;
+    float* a1ring[3] = {};
+    float* a2ring[3] = {};
     float* ring[3] = {};
     float* grad = nullptr;
     float* acc = nullptr;
@@ -289,7 +309,73 @@ struct StepIO {
     int check_step = 0;
     float* p_out = nullptr;
     cudaEvent_t wait_before_z = nullptr;  // cross-stream dependency of the pressure kernel
+    // absorbing media
+    float abs_sign = 1.f;                 // absorption_sign (-1 in the time-reversal replay)
+    float* a1_out = nullptr;              // replay: |k|^y p and |k|^(y+1) p of the new pressure
+    float* a2_out = nullptr;
 };
+
+// out = F^-1 { |k|^e F{in} } (SpectralEngine::apply_multiplier with power_multiplier(e),
+// engine.hpp:88-94,123-126), through the sim's S1 scratch spectrum.
+void apply_kpow(Ctx& c, Sim& s, const float* in, double e, float* out, cudaStream_t st) {
+    c.count(launch_zfwd(c.g, in, s.S[1], st));
+    PencilJobs j{};
+    j.buf[0] = s.S[1];
+    j.n = 1;
+    j.job[0] = {0, 0, nullptr, 0, 0.f};
+    c.count(launch_pencil(1, false, c.g, j, st));
+    j.job[0] = {0, 0, nullptr, 2, static_cast<float>(e)};
+    c.count(launch_pencil(0, false, c.g, j, st));
+    j.job[0] = {0, 0, nullptr, 0, 0.f};
+    c.count(launch_pencil(1, true, c.g, j, st));
+    c.count(launch_zinv(c.g, s.S[1], nullptr, out, st));
+}
+
+int sim_index(const Ctx& c, const Sim& s) { return &s == &c.sim[1] ? 1 : 0; }
+
+// Absorbing update_pressure (engine.hpp:327-343) after the density update and the sparse
+// work of the z pass (which left the lossless p in scratch): p = c0^2 (sum rho + s tau aout)
+// - c0^2 eta aout2, then the gathers, the replay's |k|^y / |k|^(y+1) fields, the
+// correlation and the Fy Fz p of the next step.
+void absorbing_tail(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
+    auto& sc = c.abs_s[sim_index(c, s)];
+    const long long N = c.g.N;
+    AbsArgs A{};
+    for (int a = 0; a < 3; ++a) {
+        A.rho[a] = s.rho[a];
+        A.du[a] = sc.du[a];
+    }
+    A.dtrho0 = c.dtrho0;
+    A.inv_dt = static_cast<float>(1.0 / c.grid.dt);
+    A.sum = sc.sum;
+    A.ain = sc.ain;
+    c.count(launch_abs_prep(N, A, st));
+    apply_kpow(c, s, sc.ain, c.y_pow - 2.0, sc.aout, st);
+    if (c.dispersion) apply_kpow(c, s, sc.sum, c.y_pow - 1.0, sc.aout2, st);
+    A.c0sq = c.c0sq;
+    A.tau0 = c.tau0;
+    A.eta = c.dispersion ? c.eta : nullptr;
+    A.aout = sc.aout;
+    A.aout2 = sc.aout2;
+    A.sign = io.abs_sign;
+    A.p_out = io.p_out;
+    A.check_step = io.check_step;
+    A.diverged = c.flags;
+    c.count(launch_abs_pressure(N, A, st));
+    c.count(launch_gather(io.p_out, io.sens, st));
+    c.count(launch_gather(io.p_out, io.shell, st));
+    if (io.a1_out) {
+        apply_kpow(c, s, io.p_out, c.y_pow, io.a1_out, st);
+        if (c.dispersion) apply_kpow(c, s, io.p_out, c.y_pow + 1.0, io.a2_out, st);
+    }
+    if (io.corr.grad) c.count(launch_correlate(N, io.p_out, c.c0sq, io.corr, st));
+    c.count(launch_zfwd(c.g, io.p_out, s.S[0], st));
+    PencilJobs j{};
+    j.buf[0] = s.S[0];
+    j.n = 1;
+    j.job[0] = {0, 0, nullptr, 0, 0.f};
+    c.count(launch_pencil(1, false, c.g, j, st));
+}
 
 // One leapfrog step of a stepper: update_velocity_density (engine.hpp:270-292), sparse
 // injection / shell enforcement, update_pressure (:318-347), gathers — 8 launches.
@@ -309,7 +395,7 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     const GridDev& g = c.g;
     const double SB = static_cast<double>(g.rows) * g.nzh * sizeof(float2);  // one half spectrum
     const double FB = static_cast<double>(g.N) * sizeof(float);               // one real field
-    const int ch = chunk_planes(c) > 0 ? std::min(chunk_planes(c), g.nx) : g.nx;
+    const int ch = (chunk_planes(c) > 0 && !c.absorbing) ? std::min(chunk_planes(c), g.nx) : g.nx;
     // run body(gc, frac) over the x-plane chunks
     auto chunked = [&](auto&& body) {
         for (int x0 = 0; x0 < g.nx; x0 += ch) {
@@ -378,6 +464,17 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     a.corr = io.corr;
     a.check_step = io.check_step;
     a.diverged = c.flags;
+    if (c.absorbing) {
+        // the z pass updates the densities, applies the sparse work and keeps the raw
+        // derivatives; pressure, gathers and correlation follow in absorbing_tail
+        auto& sc = c.abs_s[sim_index(c, s)];
+        for (int f = 0; f < 3; ++f) a.du_out[f] = sc.du[f];
+        a.p_out = sc.aout;
+        a.sens = SparseGather{};
+        a.shell = SparseGather{};
+        a.corr = Correlate{};
+        a.check_step = 0;
+    }
     // the fast path splits the step into the per-axis density update and the pressure
     // kernel, which re-reads the three split densities (+3F)
     const bool split = !use_generic_kernels() && fast_rows_supported(g.nz);
@@ -394,11 +491,13 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
         pencil(gc, frac, 1, true, jj);
         c.launch(KIND_ZRHO, frac * zb, [&] { return launch_zrho(gc, a, true, st); }, st);
         if (split) ++c.launches;
+        if (c.absorbing) return;
         // Y forward of Fz p for the next step
         jj.n = 1;
         jj.job[0] = {0, 0, nullptr, 0};
         pencil(gc, frac, 1, false, jj);
     });
+    if (c.absorbing) absorbing_tail(c, s, io, st);
 }
 
 // Y forward of S0 (after a pressure refresh outside run_step): restores the run_step
@@ -583,12 +682,21 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
         a.diverged = c.flags;
         c.count(launch_zrho(c.g, a, false, sb));
         y_forward_p(c, rep, sb);
+        if (c.absorbing) {  // GradientAccumulator::push of the initial value (gradient.hpp:147-160)
+            apply_kpow(c, rep, c.ring[0], c.y_pow, c.a1ring[0], sb);
+            if (c.dispersion) apply_kpow(c, rep, c.ring[0], c.y_pow + 1.0, c.a2ring[0], sb);
+        }
     }
     // look-ahead step (gradient.hpp:438-441)
     StepIO rio;
     rio.enf = SparseEnforce{n_shell, c.shell_pos, shell_row(last - 1), static_cast<float>(c.ndim)};
     rio.p_out = c.ring[1];
     rio.check_step = 0;
+    rio.abs_sign = -1.f;  // replay stepper: absorption_sign = -1 (gradient.hpp:429-431)
+    if (c.absorbing) {
+        rio.a1_out = c.a1ring[1];
+        rio.a2_out = c.a2ring[1];
+    }
     run_step(c, rep, rio, sb);
 
     StepIO aio;
@@ -604,6 +712,18 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
         rio.enf.vals = shell_row(last - n - 1);
         rio.p_out = c.ring[(n + 1) % 3];
         rio.corr = Correlate{c.ring[n % 3], c.ring[(n - 1) % 3], P[n & 1], c.grad, inv_dt};
+        if (c.absorbing) {
+            rio.a1_out = c.a1ring[(n + 1) % 3];
+            rio.a2_out = c.a2ring[(n + 1) % 3];
+            rio.corr.a1_new = c.a1ring[(n + 1) % 3];
+            rio.corr.a1_old = c.a1ring[(n - 1) % 3];
+            rio.corr.wa1 = c.wa1;
+            if (c.dispersion) {
+                rio.corr.a2_mid = c.a2ring[n % 3];
+                rio.corr.wa2 = c.wa2;
+            }
+            rio.corr.dt = static_cast<float>(c.grid.dt);
+        }
         rio.check_step = ((n + 1) & 63) == 0 ? n + 1 : 0;
         rio.wait_before_z = dual ? c.ev_adj[n & 1] : nullptr;                 // adjoint step n done
         run_step(c, rep, rio, sb);
@@ -614,6 +734,53 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
         CK(cudaStreamWaitEvent(sa, c.ev_join, 0));
     }
     c.count(launch_finalize_grad(c.grad, c.gamma, c.g.N, c.acc, accumulate ? 1 : 0, c.flags + 1, c.stream));
+}
+
+// Absorption coefficients (WaveStepper constructor engine.hpp:233-246 and the c0 branch
+// of GradientAccumulator gradient.hpp:63-74), fp32 fields; dispersion on unless y == 2
+// (engine.hpp:191). alpha0 == nullptr: lossless, scratch released.
+void set_absorption(Ctx& c, const double* alpha0, double y, const double* c0) {
+    c.release(c.abs_coef);
+    c.release(c.abs_mem);
+    c.abs_coef = c.abs_mem = nullptr;
+    c.absorbing = alpha0 != nullptr;
+    c.y_pow = y;
+    c.dispersion = c.absorbing && y != 2.0;
+    if (!c.absorbing) return;
+    const size_t N = static_cast<size_t>(c.g.N);
+    std::vector<float> h(4 * N);
+    const double tan_term = c.dispersion ? std::tan(M_PI * y / 2.0) : 0.0;
+    const double np_per_db = 100.0 * (std::log(10.0) / 20.0) / std::pow(2.0 * M_PI * 1e6, y);  // db2neper
+    for (size_t i = 0; i < N; ++i) {
+        const double a = np_per_db * alpha0[i];
+        const double cc = c0[i];
+        h[i] = static_cast<float>(-2.0 * a * std::pow(cc, y - 1.0));
+        h[N + i] = static_cast<float>(2.0 * a * std::pow(cc, y) * tan_term);
+        h[2 * N + i] = static_cast<float>(-2.0 * a * (y - 1.0) * std::pow(cc, y - 2.0));
+        h[3 * N + i] = static_cast<float>(2.0 * a * y * std::pow(cc, y - 1.0) * tan_term);
+    }
+    c.abs_coef = c.alloc<float>(4 * N);
+    CK(cudaMemcpyAsync(c.abs_coef, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+    c.tau0 = c.abs_coef;
+    c.eta = c.abs_coef + N;
+    c.wa1 = c.abs_coef + 2 * N;
+    c.wa2 = c.abs_coef + 3 * N;
+    // per stepper: du x3, ain, aout, aout2, sum; replay rings a1 x3, a2 x3
+    c.abs_mem = c.alloc<float>(20 * N);
+    float* m = c.abs_mem;
+    for (int k = 0; k < 2; ++k) {
+        auto& sc = c.abs_s[k];
+        for (int a = 0; a < 3; ++a) sc.du[a] = m + (k * 7 + a) * N;
+        sc.ain = m + (k * 7 + 3) * N;
+        sc.aout = m + (k * 7 + 4) * N;
+        sc.aout2 = m + (k * 7 + 5) * N;
+        sc.sum = m + (k * 7 + 6) * N;
+    }
+    for (int r = 0; r < 3; ++r) {
+        c.a1ring[r] = m + (14 + r) * N;
+        c.a2ring[r] = m + (17 + r) * N;
+    }
+    CK(cudaMemsetAsync(c.abs_mem, 0, 20 * N * sizeof(float), c.stream));
 }
 
 template <class Fn>
@@ -843,8 +1010,6 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
             cmax = std::max(cmax, c0[i]);
         }
         if (y <= 1.0 || y >= 3.0) fail(USTFWI_ERR_INVALID, "power-law exponent must be in (1,3)");
-        if (absorbing)
-            fail(USTFWI_ERR_INVALID, "absorbing media (alpha0 != 0) are not supported by the device engine yet");
         // WaveStepper constructor checks (engine.hpp:188-197)
         for (int a = 1; a < c->grid.ndim; ++a)
             if (c->grid.dx[a] != c->grid.dx[0])
@@ -898,6 +1063,7 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
                 c->dtr_stag[a] = Coef{dst, 0.f};
             }
         }
+        set_absorption(*c, absorbing ? alpha0 : nullptr, y, c0);
         c->gamma_host.clear();
         if (gamma) {
             c->gamma_host.assign(gamma, gamma + N);

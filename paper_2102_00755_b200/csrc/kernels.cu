@@ -50,13 +50,17 @@ __global__ void __launch_bounds__(256) pencil_pass_kernel(GridDev g, PencilJobs 
     const int n_el = L * TB;
 
     if (AXIS == 0) {
-        // kappa for the tile: k = (kx[j], ky[y], kz[c0 + c])
+        // kappa (or |k|^e) for the tile: k = (kx[j], ky[y], kz[c0 + c]); one multiplier kind
+        // per launch
         const float ky = g.ky[blockIdx.y];
+        const bool power = jobs.job[0].kappa == 2;
+        const float e = jobs.job[0].kexp;
         for (int t = threadIdx.x; t < n_el; t += blockDim.x) {
             const int j = t / TB, c = t % TB;
             const float kx = g.kx[j];
             const float kz = (c < ncol) ? g.kz[c0 + c] : 0.f;
-            kap[t] = kappa_of(kx * kx + ky * ky + kz * kz, g.half_cdt);
+            const float k2 = kx * kx + ky * ky + kz * kz;
+            kap[t] = power ? kpow_mult(k2, e) : kappa_of(k2, g.half_cdt);
         }
     }
 
@@ -261,6 +265,7 @@ __global__ void __launch_bounds__(256) zrho_kernel(GridDev g, ZrhoArgs A) {
             const float dr = A.dtrho0.at(i);
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
+                if (A.du_out[a]) A.du_out[a][i] = D[a][t];
                 float ra = A.rho[a][i];
                 ra = pm[a] * ra;
                 ra = ra - dr * D[a][t];
@@ -437,6 +442,49 @@ __global__ void scale_kernel(float* __restrict__ a, long long n, float s) {
 }
 
 // ---------------------------------------------------------------------------------
+// Absorbing media (engine.hpp:327-343) and the stand-alone correlation / gathers
+// ---------------------------------------------------------------------------------
+__global__ void abs_prep_kernel(long long n, AbsArgs A) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        A.sum[i] = (A.rho[0][i] + A.rho[1][i]) + A.rho[2][i];
+        A.ain[i] = (A.dtrho0.at(i) * A.inv_dt) * ((A.du[0][i] + A.du[1][i]) + A.du[2][i]);
+    }
+}
+
+__global__ void abs_pressure_kernel(long long n, AbsArgs A) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float c2 = A.c0sq[i];
+        float p = c2 * (A.sum[i] + (A.sign * A.tau0[i]) * A.aout[i]);
+        if (A.eta) p -= c2 * A.eta[i] * A.aout2[i];
+        A.p_out[i] = p;
+        if (A.check_step > 0 && i == 0 && !isfinite(p)) atomicMin(A.diverged, A.check_step);
+    }
+}
+
+// GradientAccumulator::accumulate, c0 branch (gradient.hpp:177-203)
+__global__ void correlate_kernel(long long n, const float* __restrict__ p_new, const float* __restrict__ c0sq,
+                                 Correlate C) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float c2 = c0sq[i];
+        const float q = C.q_adj[i];
+        const float w = 2.f / (c2 * sqrtf(c2));
+        float gv = C.grad[i];
+        gv += w * (((p_new[i] - 2.f * C.p_mid[i]) + C.p_old[i]) * C.inv_dt) * q;
+        if (C.a1_new) gv += C.wa1[i] * (0.5f * (C.a1_old[i] - C.a1_new[i])) * q;
+        if (C.a2_mid) gv += C.wa2[i] * C.a2_mid[i] * q * C.dt;
+        C.grad[i] = gv;
+    }
+}
+
+__global__ void gather_kernel(const float* __restrict__ p, SparseGather G) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < G.n) G.out[G.idx ? G.idx[s] : s] = p[G.pos[s]];
+}
+
+// ---------------------------------------------------------------------------------
 // Host-callable launchers
 // ---------------------------------------------------------------------------------
 
@@ -566,6 +614,27 @@ cudaError_t launch_check_finite(const float* a, long long n, int* flag, cudaStre
 
 cudaError_t launch_scale(float* a, long long n, float s, cudaStream_t st) {
     scale_kernel<<<flat_blocks(n), 256, 0, st>>>(a, n, s);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_abs_prep(long long n, const AbsArgs& a, cudaStream_t st) {
+    abs_prep_kernel<<<flat_blocks(n), 256, 0, st>>>(n, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_abs_pressure(long long n, const AbsArgs& a, cudaStream_t st) {
+    abs_pressure_kernel<<<flat_blocks(n), 256, 0, st>>>(n, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_correlate(long long n, const float* p_new, const float* c0sq, const Correlate& c, cudaStream_t st) {
+    correlate_kernel<<<flat_blocks(n), 256, 0, st>>>(n, p_new, c0sq, c);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const float* p, const SparseGather& g, cudaStream_t st) {
+    if (g.n <= 0) return cudaSuccess;
+    gather_kernel<<<(g.n + 255) / 256, 256, 0, st>>>(p, g);
     return cudaGetLastError();
 }
 

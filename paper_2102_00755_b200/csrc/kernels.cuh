@@ -69,6 +69,14 @@ struct Correlate {
     const float* q_adj;
     float* grad;
     float inv_dt;
+    // absorbing media (gradient.hpp:63-74,183-203): grad += wa1 * (a1_old - a1_new)/2 * q
+    // + wa2 * a2_mid * q * dt with a1 = |k|^y p, a2 = |k|^(y+1) p of the replay pressures
+    const float* a1_new = nullptr;
+    const float* a1_old = nullptr;
+    const float* a2_mid = nullptr;
+    const float* wa1 = nullptr;
+    const float* wa2 = nullptr;
+    float dt = 0.f;
 };
 
 // Per-axis PML profiles (make_pml, grid.hpp:153-178), fp32.
@@ -89,8 +97,16 @@ struct PencilJob {
     int src;              // scratch buffer index read
     int dst;              // scratch buffer index written
     const float2* dmul;   // per-index factor along the pass axis (D_a table), nullable
-    int kappa;            // X pass only: multiply by kappa(|k|)
+    int kappa;            // X pass only: 1 multiply by kappa(|k|), 2 by |k|^kexp (power_multiplier)
+    float kexp;           // exponent of |k| for kappa == 2 (engine.hpp:88-94)
 };
+
+// power_multiplier (engine.hpp:88-94): |k|^e over the half spectrum, the k = 0 bin 1 for
+// e == 0 and 0 otherwise (fractional-Laplacian convention)
+__device__ __forceinline__ float kpow_mult(float k2, float e) {
+    if (k2 == 0.f) return e == 0.f ? 1.f : 0.f;
+    return powf(k2, 0.5f * e);
+}
 
 struct PencilJobs {
     int n;
@@ -116,6 +132,29 @@ struct ZrhoArgs {
     int check_step;       // >0: divergence check of p[0] at this stepper step index
     int* diverged;        // atomicMin of the failing step index
     int rows_per_cta;
+    float* du_out[3];     // absorbing media: the raw derivative d_a^- v_a (engine.hpp:285), nullable
+};
+
+// Absorbing pressure (update_pressure, engine.hpp:327-343), after the sparse work:
+//   sum = sum_a rho_a, ain = (dt rho0 / dt) sum_a du_a       (abs_prep)
+//   p = c0^2 (sum + sign tau0 aout) - c0^2 eta aout2           (abs_pressure)
+// with aout = |k|^(y-2) ain and aout2 = |k|^(y-1) sum applied spectrally in between.
+struct AbsArgs {
+    const float* rho[3];
+    const float* du[3];
+    Coef dtrho0;
+    float inv_dt;
+    float* sum;
+    float* ain;
+    const float* c0sq;
+    const float* tau0;
+    const float* eta;     // nullptr: no dispersion term
+    const float* aout;
+    const float* aout2;
+    float sign;           // absorption_sign (+1 forward / adjoint, -1 replay, gradient.hpp:429-431)
+    float* p_out;
+    int check_step;
+    int* diverged;
 };
 
 
@@ -135,6 +174,10 @@ cudaError_t launch_finalize_grad(const float* grad, const uint8_t* gamma, long l
                                  int* nonfinite, cudaStream_t st);
 cudaError_t launch_check_finite(const float* a, long long n, int* flag, cudaStream_t st);
 cudaError_t launch_scale(float* a, long long n, float s, cudaStream_t st);
+cudaError_t launch_abs_prep(long long n, const AbsArgs& a, cudaStream_t st);
+cudaError_t launch_abs_pressure(long long n, const AbsArgs& a, cudaStream_t st);
+cudaError_t launch_correlate(long long n, const float* p_new, const float* c0sq, const Correlate& c, cudaStream_t st);
+cudaError_t launch_gather(const float* p, const SparseGather& g, cudaStream_t st);
 
 // register-resident fast paths (passes.cu) for the compiled transform lengths
 bool fast_pencil_supported(int L);

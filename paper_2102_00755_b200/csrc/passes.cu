@@ -237,14 +237,17 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
                 forward(X);
                 if (inB) {
                     if (kap && w.grp == 0) {
-                        // kappa(|k|) of this tile, evaluated once for all its source groups
+                        // kappa(|k|) (or |k|^e) of this tile, evaluated once for all its source groups
                         const float ky = g.ky[w.line];
                         const float kz = colok ? g.kz[w.c0 + c] : 0.f;
+                        const bool power = jobs.job[gstart[w.grp]].kappa == 2;
+                        const float e = jobs.job[gstart[w.grp]].kexp;
 #pragma unroll
                         for (int k2 = 0; k2 < N2; ++k2) {
                             const int k = C::out_row(kb, k2);
                             const float kx = g.kx[k];
-                            kap_s[k * TB + c] = kappa_fast(kx * kx + ky * ky + kz * kz, g.half_cdt);
+                            const float q2 = kx * kx + ky * ky + kz * kz;
+                            kap_s[k * TB + c] = power ? kpow_mult(q2, e) : kappa_fast(q2, g.half_cdt);
                         }
                     }
 #pragma unroll
@@ -436,11 +439,14 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
                     if (grp == 0) {
                         const float ky = g.ky[line];
                         const float kz = col0 + c < g.nzh ? g.kz[col0 + c] : 0.f;
+                        const bool power = jobs.job[gb].kappa == 2;  // one multiplier kind per launch
+                        const float e = jobs.job[gb].kexp;
 #pragma unroll
                         for (int k2 = 0; k2 < N2; ++k2) {
                             const int k = C::out_row(kb, k2);
                             const float kx = g.kx[k];
-                            kap_s[k * TB + c] = kappa_fast(kx * kx + ky * ky + kz * kz, g.half_cdt);
+                            const float q2 = kx * kx + ky * ky + kz * kz;
+                            kap_s[k * TB + c] = power ? kpow_mult(q2, e) : kappa_fast(q2, g.half_cdt);
                         }
                     }
 #pragma unroll
@@ -715,6 +721,7 @@ __global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zrho_axis_kernel(const 
             if (a == 2) pm = *reinterpret_cast<const float2*>(A.pml.prof[2] + 2 * n);
             float2 d = make_float2(dsc, dsc);
             if (coef_field) d = *reinterpret_cast<const float2*>(ds + 2 * n);
+            if (A.du_out[a]) *reinterpret_cast<float2*>(A.du_out[a] + row * NZ + 2 * n) = u[n1];
             q.x = pm.x * (pm.x * q.x - d.x * u[n1].x);
             q.y = pm.y * (pm.y * q.y - d.y * u[n1].y);
             *reinterpret_cast<float2*>(rg + 2 * n) = q;
@@ -1156,6 +1163,7 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const _
                 if (a == 2) pm = __ldg(reinterpret_cast<const float2*>(A.pml.prof[2]) + n);
                 float2 d = make_float2(dsc, dsc);
                 if (coef_field) d = *reinterpret_cast<const float2*>(ds + 2 * n);
+                if (A.du_out[a]) *reinterpret_cast<float2*>(A.du_out[a] + row * NZ + 2 * n) = u[n1];
                 q.x = pm.x * (pm.x * q.x - d.x * u[n1].x);
                 q.y = pm.y * (pm.y * q.y - d.y * u[n1].y);
                 *reinterpret_cast<float2*>(ra + row * NZ + 2 * n) = q;
@@ -1247,44 +1255,30 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zp2_kernel(const __grid_c
 
     float2 pv[NA][N1];
     if (rowok) {
-        // loads of a chunk of pairs are issued before any store of the chunk (the output
-        // pointers may alias the inputs as far as the compiler knows)
-        constexpr int CH = N1 % 4 == 0 ? 4 : (N1 % 2 == 0 ? 2 : 1);
-        const bool corr = A.corr.grad != nullptr;
 #pragma unroll
         for (int j = 0; j < NA; ++j) {
             const int n2 = t + TPR * j;
 #pragma unroll
-            for (int h = 0; h < N1; h += CH) {
-                float2 q0[CH], q1[CH], q2[CH], c2[CH], pm[CH], po[CH], qa[CH], gv[CH];
-#pragma unroll
-                for (int e = 0; e < CH; ++e) {
-                    const long long i = row * NZ + 2 * (n2 + N2 * (h + e));
-                    q0[e] = *reinterpret_cast<const float2*>(A.rho[0] + i);
-                    q1[e] = *reinterpret_cast<const float2*>(A.rho[1] + i);
-                    q2[e] = *reinterpret_cast<const float2*>(A.rho[2] + i);
-                    c2[e] = __ldg(reinterpret_cast<const float2*>(A.c0sq + i));
-                    if (corr) {
-                        pm[e] = __ldg(reinterpret_cast<const float2*>(A.corr.p_mid + i));
-                        po[e] = __ldg(reinterpret_cast<const float2*>(A.corr.p_old + i));
-                        qa[e] = __ldg(reinterpret_cast<const float2*>(A.corr.q_adj + i));
-                        gv[e] = *reinterpret_cast<const float2*>(A.corr.grad + i);
-                    }
-                }
-#pragma unroll
-                for (int e = 0; e < CH; ++e) {
-                    const long long i = row * NZ + 2 * (n2 + N2 * (h + e));
-                    float2 p;
-                    p.x = c2[e].x * ((q0[e].x + q1[e].x) + q2[e].x);
-                    p.y = c2[e].y * ((q0[e].y + q1[e].y) + q2[e].y);
-                    *reinterpret_cast<float2*>(A.p_out + i) = p;
-                    pv[j][h + e] = p;
-                    if (corr) {
-                        const float wx = 2.f / (c2[e].x * sqrtf(c2[e].x)), wy = 2.f / (c2[e].y * sqrtf(c2[e].y));
-                        gv[e].x += wx * (((p.x - 2.f * pm[e].x) + po[e].x) * A.corr.inv_dt) * qa[e].x;
-                        gv[e].y += wy * (((p.y - 2.f * pm[e].y) + po[e].y) * A.corr.inv_dt) * qa[e].y;
-                        *reinterpret_cast<float2*>(A.corr.grad + i) = gv[e];
-                    }
+            for (int n1 = 0; n1 < N1; ++n1) {
+                const long long i = row * NZ + 2 * (n2 + N2 * n1);
+                const float2 q0 = *reinterpret_cast<const float2*>(A.rho[0] + i);
+                const float2 q1 = *reinterpret_cast<const float2*>(A.rho[1] + i);
+                const float2 q2 = *reinterpret_cast<const float2*>(A.rho[2] + i);
+                const float2 c2 = __ldg(reinterpret_cast<const float2*>(A.c0sq + i));
+                float2 p;
+                p.x = c2.x * ((q0.x + q1.x) + q2.x);
+                p.y = c2.y * ((q0.y + q1.y) + q2.y);
+                *reinterpret_cast<float2*>(A.p_out + i) = p;
+                pv[j][n1] = p;
+                if (A.corr.grad != nullptr) {
+                    const float2 pm = *reinterpret_cast<const float2*>(A.corr.p_mid + i);
+                    const float2 po = *reinterpret_cast<const float2*>(A.corr.p_old + i);
+                    const float2 qa = *reinterpret_cast<const float2*>(A.corr.q_adj + i);
+                    float2 gv = *reinterpret_cast<const float2*>(A.corr.grad + i);
+                    const float wx = 2.f / (c2.x * sqrtf(c2.x)), wy = 2.f / (c2.y * sqrtf(c2.y));
+                    gv.x += wx * (((p.x - 2.f * pm.x) + po.x) * A.corr.inv_dt) * qa.x;
+                    gv.y += wy * (((p.y - 2.f * pm.y) + po.y) * A.corr.inv_dt) * qa.y;
+                    *reinterpret_cast<float2*>(A.corr.grad + i) = gv;
                 }
             }
         }

@@ -11,6 +11,9 @@ Fixtures (small, committed):
   config_a.npz        config A (64^3, nt=393): observed data (truth medium), model traces,
                       subsampled shell trace, TR gradient on gamma and loss
   config_a_short.npz  config A truncated to nt=96 with f_obs = 0 (fast GPU parity case)
+  config_a_absorb.npz config A at nt=96 with power-law absorption (alpha0 3 dB/(MHz^y cm) in
+                      gamma, 0.5 outside): y = 1.5 traces + TR gradient + loss (f_obs = 0),
+                      y = 2 (no dispersion term) traces
 """
 from __future__ import annotations
 
@@ -95,11 +98,43 @@ def config_a_fixture(nt, name, trace_stride=(8, 16), observed_zero=False):
     print(f"{name}: fwd {t1 - t0:.1f}s fwd+trace {t2 - t1:.1f}s gradient {t3 - t2:.1f}s loss {loss:.6e}")
 
 
+def absorbing_medium(m, y):
+    import copy
+    a = copy.copy(m)
+    gam = np.asarray(m.gamma, bool)
+    a.alpha0 = np.where(gam, 3.0, 0.5)
+    a.y = y
+    return a
+
+
+def config_a_absorb_fixture(nt=96):
+    sc = scenario.config_a(nt=nt)
+    g = sc.grid
+    pos, sig = list(sc.sources.positions), [np.asarray(s) for s in sc.sources.signals]
+    m15 = absorbing_medium(sc.model, 1.5)
+    m20 = absorbing_medium(sc.model, 2.0)
+    observed = np.zeros((len(sc.sensors.positions), g.nt))
+    data15, trace = ref.simulate_forward(g, m15, pos, sig, sc.sensors.positions, boundary_thickness=8)
+    data20, _ = ref.simulate_forward(g, m20, pos, sig, sc.sensors.positions)
+    lossless, _ = ref.simulate_forward(g, sc.model, pos, sig, sc.sensors.positions)
+    loss, grad = ref.gradient_time_reversal(g, m15, pos, sig, sc.sensors.positions, observed, 8)
+    gidx = np.flatnonzero(np.asarray(sc.model.gamma).ravel())
+    np.savez_compressed(os.path.join(OUT, "config_a_absorb.npz"), nt=g.nt, data_y15=data15, data_y20=data20,
+                        data_lossless=lossless, trace_checksum=np.array([trace.sum(), np.abs(trace).sum()]),
+                        loss=loss, grad_gamma=grad.ravel()[gidx], gamma_idx=gidx)
+    print(f"config_a_absorb: loss {loss:.6e}, |abs - lossless| / |lossless| = "
+          f"{np.linalg.norm(data15 - lossless) / np.linalg.norm(lossless):.3e}")
+
+
 if __name__ == "__main__":
+    if "--absorb-only" in sys.argv:
+        config_a_absorb_fixture()
+        sys.exit(0)
     if not ref.available():
         sys.exit("oracle/_ref missing: make -C oracle")
     derivative_fixture()
     forward_2d_fixture()
     config_a_fixture(96, "config_a_short", observed_zero=True)
+    config_a_absorb_fixture()
     if "--quick" not in sys.argv:
         config_a_fixture(None, "config_a")

@@ -227,8 +227,12 @@ def test_error_mapping():
         bad.c0 = np.full(g.shape, 1900.0)        # outside [c0_min, c0_max]
         with pytest.raises(ValueError):
             eng.set_medium(bad)
-        lossy = make_homogeneous_medium(g, 1500.0, alpha0=0.5)
-        with pytest.raises(ValueError):
+        lossy = make_homogeneous_medium(g, 1500.0, alpha0=0.5, y=3.0)  # y outside (1,3), medium.hpp:52
+        with pytest.raises(ValueError, match="power-law exponent"):
+            eng.set_medium(lossy)
+        lossy.alpha0 = np.full(g.shape, -0.5)
+        lossy.y = 1.5
+        with pytest.raises(ValueError, match="alpha0 must be non-negative"):
             eng.set_medium(lossy)
     g.dt = 1e-3 / 1500.0  # cfl = 1 > 2/pi (test_solver.cpp:352-358)
     with GpuEngine(g) as eng:
