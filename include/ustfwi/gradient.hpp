@@ -63,6 +63,7 @@ inline GradientResult compute_gradient(const Medium& medium, const SourceSet& so
     engine->bind(sensors);
     GradientResult r;
     r.grad = Field(grid.dims);
+    detail::check(ustfwi_gpu_set_gradient_options(engine->ctx(), opt.dispersion_enabled ? 1 : 0));
     detail::check(ustfwi_gpu_gradient_tr(engine->ctx(), observed.samples.data(), opt.boundary_thickness, r.grad.data(),
                                          &r.loss));
     r.param = param;

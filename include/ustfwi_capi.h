@@ -113,6 +113,11 @@ USTFWI_API int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* ctx, const double* c0, cons
                           const double* alpha0, double y, const uint8_t* gamma, double c0_min,
                           double c0_max);
 
+/* GradientOptions::dispersion_enabled (adjoint/gradient.hpp:22-32): the dispersion term of the
+ * adjoint and time-reversal steppers and of the gradient's absorption terms (gradient.hpp:56,
+ * 381-384, 424-426); the forward simulation keeps it (default StepperOptions). Default 1. */
+USTFWI_API int ustfwi_gpu_set_gradient_options(ustfwi_gpu_ctx* ctx, int dispersion_enabled);
+
 /* SourceSet (solver/medium.hpp:74-85), generalised to encoded super-sources: source i fires
  * at flat index pos[i] with sample(i, n) = w_i * sig[sig_off[i] + n - delay_i] when
  * 0 <= n - delay_i < sig_off[i+1] - sig_off[i], else 0. weights / delay_steps may be NULL

@@ -255,6 +255,22 @@ def gradient_time_reversal(g, medium, positions, signals, sensors, observed, thi
     return loss.value, grad
 
 
+def gradient_tr_opts(g, medium, positions, signals, sensors, observed, thickness, dispersion_enabled=True):
+    """compute_gradient (gradient.hpp:333-464), TR method, with GradientOptions::dispersion_enabled."""
+    keep: list = []
+    s = grid_struct(g)
+    m = _medium(medium, keep)
+    src = _sources(positions, signals, keep)
+    sens = np.ascontiguousarray(sensors, dtype=np.uint64)
+    obs = np.ascontiguousarray(observed, dtype=np.float64)
+    grad = np.zeros(tuple(g.dims[a] for a in range(int(getattr(g, "ndim", len(g.dims))))))
+    loss = C.c_double(0.0)
+    _check(lib().ref_gradient_tr_opts(C.byref(s), C.byref(m), C.byref(src), C.c_size_t(len(sens)),
+                                      _p(sens, C.c_size_t), _p(obs, C.c_double), thickness,
+                                      int(bool(dispersion_enabled)), _p(grad, C.c_double), C.byref(loss)))
+    return loss.value, grad
+
+
 def evaluate_loss(g, medium, positions, signals, sensors, observed):
     keep: list = []
     s = grid_struct(g)

@@ -132,7 +132,9 @@ struct ustfwi_gpu_ctx {
     // absorbing media (engine.hpp:233-246; gradient.hpp:63-74): coefficient fields and
     // per-stepper scratch, allocated only when alpha0 != 0
     bool absorbing = false;
-    bool dispersion = false;
+    bool dispersion = false;       // y != 2 (engine.hpp:191)
+    bool grad_dispersion = true;   // GradientOptions::dispersion_enabled (adjoint + replay)
+    bool disp_active = false;      // dispersion term of the stepper currently running
     double y_pow = 1.5;
     float* abs_coef = nullptr;     // tau0, eta, wa1, wa2 (4 fields)
     float* tau0 = nullptr;
@@ -351,10 +353,10 @@ void absorbing_tail(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     A.ain = sc.ain;
     c.count(launch_abs_prep(N, A, st));
     apply_kpow(c, s, sc.ain, c.y_pow - 2.0, sc.aout, st);
-    if (c.dispersion) apply_kpow(c, s, sc.sum, c.y_pow - 1.0, sc.aout2, st);
+    if (c.disp_active) apply_kpow(c, s, sc.sum, c.y_pow - 1.0, sc.aout2, st);
     A.c0sq = c.c0sq;
     A.tau0 = c.tau0;
-    A.eta = c.dispersion ? c.eta : nullptr;
+    A.eta = c.disp_active ? c.eta : nullptr;
     A.aout = sc.aout;
     A.aout2 = sc.aout2;
     A.sign = io.abs_sign;
@@ -366,7 +368,7 @@ void absorbing_tail(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     c.count(launch_gather(io.p_out, io.shell, st));
     if (io.a1_out) {
         apply_kpow(c, s, io.p_out, c.y_pow, io.a1_out, st);
-        if (c.dispersion) apply_kpow(c, s, io.p_out, c.y_pow + 1.0, io.a2_out, st);
+        if (c.disp_active) apply_kpow(c, s, io.p_out, c.y_pow + 1.0, io.a2_out, st);
     }
     if (io.corr.grad) c.count(launch_correlate(N, io.p_out, c.c0sq, io.corr, st));
     c.count(launch_zfwd(c.g, io.p_out, s.S[0], st));
@@ -613,6 +615,7 @@ void forward_sim(Ctx& c, int thickness) {
     ensure_data_buffers(c);
     if (thickness > 0) prepare_shell(c, thickness);
     refresh_scales(c, c.src);
+    c.disp_active = c.dispersion;  // simulate_forward: default StepperOptions
     Sim& s = c.sim[0];
     reset_sim(c, s, true);
     const int nt = c.grid.nt;
@@ -640,6 +643,7 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
     if (thickness < 1) fail(USTFWI_ERR_INVALID, "shell thickness must be >= 1");
     const int nt = c.grid.nt, ns = c.n_sens, last = nt - 1;
     forward_sim(c, thickness);
+    c.disp_active = c.dispersion && c.grad_dispersion;  // adjoint + replay steppers (gradient.hpp:381,424-426)
     // adjoint source: reverse, Kahan loss, integrate (gradient.hpp:264-289,378-379)
     c.count(launch_adjoint_source(c.data, c.obs, nt, ns, 1, c.q, c.loss_part, c.loss, c.loss + 1,
                                   accumulate ? 1 : 0, c.stream));
@@ -684,7 +688,7 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
         y_forward_p(c, rep, sb);
         if (c.absorbing) {  // GradientAccumulator::push of the initial value (gradient.hpp:147-160)
             apply_kpow(c, rep, c.ring[0], c.y_pow, c.a1ring[0], sb);
-            if (c.dispersion) apply_kpow(c, rep, c.ring[0], c.y_pow + 1.0, c.a2ring[0], sb);
+            if (c.disp_active) apply_kpow(c, rep, c.ring[0], c.y_pow + 1.0, c.a2ring[0], sb);
         }
     }
     // look-ahead step (gradient.hpp:438-441)
@@ -718,7 +722,7 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
             rio.corr.a1_new = c.a1ring[(n + 1) % 3];
             rio.corr.a1_old = c.a1ring[(n - 1) % 3];
             rio.corr.wa1 = c.wa1;
-            if (c.dispersion) {
+            if (c.disp_active) {
                 rio.corr.a2_mid = c.a2ring[n % 3];
                 rio.corr.wa2 = c.wa2;
             }
@@ -1074,6 +1078,10 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
         c->has_medium = true;
         CK(cudaStreamSynchronize(c->stream));
     });
+}
+
+int ustfwi_gpu_set_gradient_options(ustfwi_gpu_ctx* c, int dispersion_enabled) {
+    return guarded(c, [&] { c->grad_dispersion = dispersion_enabled != 0; });
 }
 
 int ustfwi_gpu_set_sources(ustfwi_gpu_ctx* c, size_t n_src, const size_t* pos, const size_t* sig_off,

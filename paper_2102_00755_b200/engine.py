@@ -190,11 +190,13 @@ class GpuEngine:
                                                  C.byref(loss)))
         return loss.value, grad
 
-    def gradient_tr(self, observed: np.ndarray, thickness: int):
-        """-> (loss, grad) ; grad zero outside gamma."""
+    def gradient_tr(self, observed: np.ndarray, thickness: int, dispersion_enabled: bool = True):
+        """-> (loss, grad) ; grad zero outside gamma. dispersion_enabled: GradientOptions
+        (gradient.hpp:31), the adjoint / replay dispersion term of absorbing media."""
         obs = np.ascontiguousarray(observed, dtype=np.float64)
         if obs.shape != (self.n_sensors, self.grid.nt):
             raise ValueError("observed data dimensions do not match the simulation")
+        check(lib().ustfwi_gpu_set_gradient_options(self._h, int(bool(dispersion_enabled))))
         grad = np.zeros(self.grid.shape)
         loss = C.c_double(0.0)
         check(lib().ustfwi_gpu_gradient_tr(self._h, ptr(obs, C.c_double), int(thickness), ptr(grad, C.c_double),

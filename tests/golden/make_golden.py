@@ -12,8 +12,9 @@ Fixtures (small, committed):
                       subsampled shell trace, TR gradient on gamma and loss
   config_a_short.npz  config A truncated to nt=96 with f_obs = 0 (fast GPU parity case)
   config_a_absorb.npz config A at nt=96 with power-law absorption (alpha0 3 dB/(MHz^y cm) in
-                      gamma, 0.5 outside): y = 1.5 traces + TR gradient + loss (f_obs = 0),
-                      y = 2 (no dispersion term) traces
+                      gamma, 0.5 outside): y = 1.5 traces + TR gradient + loss (f_obs = 0), the
+                      same gradient with GradientOptions::dispersion_enabled = false, y = 2 (no
+                      dispersion term) traces
 """
 from __future__ import annotations
 
@@ -118,10 +119,13 @@ def config_a_absorb_fixture(nt=96):
     data20, _ = ref.simulate_forward(g, m20, pos, sig, sc.sensors.positions)
     lossless, _ = ref.simulate_forward(g, sc.model, pos, sig, sc.sensors.positions)
     loss, grad = ref.gradient_time_reversal(g, m15, pos, sig, sc.sensors.positions, observed, 8)
+    loss_nd, grad_nd = ref.gradient_tr_opts(g, m15, pos, sig, sc.sensors.positions, observed, 8,
+                                            dispersion_enabled=False)
     gidx = np.flatnonzero(np.asarray(sc.model.gamma).ravel())
     np.savez_compressed(os.path.join(OUT, "config_a_absorb.npz"), nt=g.nt, data_y15=data15, data_y20=data20,
                         data_lossless=lossless, trace_checksum=np.array([trace.sum(), np.abs(trace).sum()]),
-                        loss=loss, grad_gamma=grad.ravel()[gidx], gamma_idx=gidx)
+                        loss=loss, grad_gamma=grad.ravel()[gidx], gamma_idx=gidx,
+                        loss_nodisp=loss_nd, grad_gamma_nodisp=grad_nd.ravel()[gidx])
     print(f"config_a_absorb: loss {loss:.6e}, |abs - lossless| / |lossless| = "
           f"{np.linalg.norm(data15 - lossless) / np.linalg.norm(lossless):.3e}")
 

@@ -68,6 +68,20 @@ def test_absorbing_tr_gradient(setup):
     assert rel(grad.ravel()[z["gamma_idx"]], z["grad_gamma"]) < GRAD_TOL
 
 
+def test_absorbing_tr_gradient_dispersion_disabled(setup):
+    # GradientOptions::dispersion_enabled = false: adjoint and replay drop the dispersion
+    # term, the forward simulation keeps it (gradient.hpp:381-384,424-426)
+    sc, z, eng = setup
+    eng.set_medium(absorbing(sc.model, 1.5))
+    observed = np.zeros((len(sc.sensors.positions), int(z["nt"])))
+    loss, grad = eng.gradient_tr(observed, 8, dispersion_enabled=False)
+    assert abs(loss - float(z["loss_nodisp"])) <= 1e-4 * abs(float(z["loss_nodisp"]))
+    g = grad.ravel()[z["gamma_idx"]]
+    assert rel(g, z["grad_gamma_nodisp"]) < GRAD_TOL
+    # the switch matters at this tolerance
+    assert rel(z["grad_gamma_nodisp"], z["grad_gamma"]) > 10 * GRAD_TOL
+
+
 def test_lossless_after_absorbing_medium(setup, golden):
     # switching back to alpha0 = None releases the absorbing path
     sc, z, eng = setup
