@@ -191,6 +191,22 @@ USTFWI_API int ustfwi_gpu_comm_init(ustfwi_gpu_ctx* ctx, const char id[128], int
 /* In place: accumulator <- (sum over ranks of accumulator) / batch, loss likewise. */
 USTFWI_API int ustfwi_gpu_allreduce_mean(ustfwi_gpu_ctx* ctx, int batch);
 
+/* ---- SLBFGS curvature history on the device (Algorithm 2 / Appendix D; SPEC.md
+ * optimizer: two_loop_recursion, LbfgsState with m_h = 64). fp64 vectors of length n; S, Y
+ * rings, rho_i and H0 = gamma I (gamma = <s,y>/<y,y> of the newest pair) stay in HBM. ---- */
+typedef struct ustfwi_lbfgs ustfwi_lbfgs;
+USTFWI_API int ustfwi_lbfgs_create(int device, size_t n, int history, ustfwi_lbfgs** out);
+USTFWI_API int ustfwi_lbfgs_destroy(ustfwi_lbfgs* h);
+/* Forget all pairs (H0 = I). */
+USTFWI_API int ustfwi_lbfgs_reset(ustfwi_lbfgs* h);
+/* updateBuffer(s, S), updateBuffer(y, Y) (Algorithm 2); the pair is rejected (*accepted = 0)
+ * unless <s,y> > reject_tol * |s| |y| (SPEC design decision, default 1e-10). Host vectors. */
+USTFWI_API int ustfwi_lbfgs_push(ustfwi_lbfgs* h, const double* s, const double* y, double reject_tol, int* accepted);
+/* out = H_k g by the two-loop recursion (empty history: g). Host vectors. */
+USTFWI_API int ustfwi_lbfgs_apply(ustfwi_lbfgs* h, const double* g, double* out);
+/* Number of stored pairs and the current H0 scaling. */
+USTFWI_API int ustfwi_lbfgs_pairs(const ustfwi_lbfgs* h, int* count, double* gamma);
+
 #ifdef __cplusplus
 }
 #endif
