@@ -39,7 +39,7 @@ struct GradientResult {
     int n_simulations = 0;
 };
 
-/// adjoint/gradient.hpp:333-464 (time-reversal branch, GradientParam::c0)
+/// adjoint/gradient.hpp:333-464 (time-reversal branch, GradientParam c0 / alpha0 / y)
 inline GradientResult compute_gradient(const Medium& medium, const SourceSet& source, const SensorArray& sensors,
                                        const SensorData& observed, const Grid& grid, GradientParam param,
                                        const GradientOptions& opt = {}, SpectralEngine* engine = nullptr) {
@@ -48,7 +48,8 @@ inline GradientResult compute_gradient(const Medium& medium, const SourceSet& so
     if (observed.nt != grid.nt) throw std::invalid_argument("observed data length does not match the grid");
     if (observed.n_sensors != static_cast<int>(sensors.count()))
         throw std::invalid_argument("observed data dimensions do not match the simulation");
-    if (param != GradientParam::c0) throw std::invalid_argument("the device engine computes the c0 gradient only");
+    if (param == GradientParam::rho0)
+        throw std::invalid_argument("the device engine does not provide the rho0 gradient (defective reference branch)");
     if (opt.method != GradientMethod::time_reversal)
         throw std::invalid_argument("the device engine implements the time-reversal gradient method");
     if (!opt.source_integration_correction)
@@ -64,6 +65,9 @@ inline GradientResult compute_gradient(const Medium& medium, const SourceSet& so
     GradientResult r;
     r.grad = Field(grid.dims);
     detail::check(ustfwi_gpu_set_gradient_options(engine->ctx(), opt.dispersion_enabled ? 1 : 0));
+    detail::check(ustfwi_gpu_set_gradient_param(
+        engine->ctx(), param == GradientParam::alpha0 ? USTFWI_PARAM_ALPHA0
+                                                      : (param == GradientParam::y ? USTFWI_PARAM_Y : USTFWI_PARAM_C0)));
     detail::check(ustfwi_gpu_gradient_tr(engine->ctx(), observed.samples.data(), opt.boundary_thickness, r.grad.data(),
                                          &r.loss));
     r.param = param;

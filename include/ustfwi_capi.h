@@ -118,6 +118,15 @@ USTFWI_API int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* ctx, const double* c0, cons
  * 381-384, 424-426); the forward simulation keeps it (default StepperOptions). Default 1. */
 USTFWI_API int ustfwi_gpu_set_gradient_options(ustfwi_gpu_ctx* ctx, int dispersion_enabled);
 
+/* GradientParam of the next gradient (adjoint/gradient.hpp:9, GradientAccumulator :50-142):
+ * USTFWI_PARAM_C0 (default), USTFWI_PARAM_ALPHA0, USTFWI_PARAM_Y. USTFWI_PARAM_RHO0 is
+ * rejected with USTFWI_ERR_INVALID (the reference branch is defective). */
+#define USTFWI_PARAM_C0 0
+#define USTFWI_PARAM_RHO0 1
+#define USTFWI_PARAM_ALPHA0 2
+#define USTFWI_PARAM_Y 3
+USTFWI_API int ustfwi_gpu_set_gradient_param(ustfwi_gpu_ctx* ctx, int param);
+
 /* SourceSet (solver/medium.hpp:74-85), generalised to encoded super-sources: source i fires
  * at flat index pos[i] with sample(i, n) = w_i * sig[sig_off[i] + n - delay_i] when
  * 0 <= n - delay_i < sig_off[i+1] - sig_off[i], else 0. weights / delay_steps may be NULL

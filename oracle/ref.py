@@ -255,8 +255,13 @@ def gradient_time_reversal(g, medium, positions, signals, sensors, observed, thi
     return loss.value, grad
 
 
-def gradient_tr_opts(g, medium, positions, signals, sensors, observed, thickness, dispersion_enabled=True):
-    """compute_gradient (gradient.hpp:333-464), TR method, with GradientOptions::dispersion_enabled."""
+PARAM = {"c0": 0, "rho0": 1, "alpha0": 2, "y": 3}
+
+
+def gradient_tr_opts(g, medium, positions, signals, sensors, observed, thickness, dispersion_enabled=True,
+                     param="c0"):
+    """compute_gradient (gradient.hpp:333-464), TR method, GradientParam, with
+    GradientOptions::dispersion_enabled."""
     keep: list = []
     s = grid_struct(g)
     m = _medium(medium, keep)
@@ -267,7 +272,8 @@ def gradient_tr_opts(g, medium, positions, signals, sensors, observed, thickness
     loss = C.c_double(0.0)
     _check(lib().ref_gradient_tr_opts(C.byref(s), C.byref(m), C.byref(src), C.c_size_t(len(sens)),
                                       _p(sens, C.c_size_t), _p(obs, C.c_double), thickness,
-                                      int(bool(dispersion_enabled)), _p(grad, C.c_double), C.byref(loss)))
+                                      int(bool(dispersion_enabled)), PARAM[param], _p(grad, C.c_double),
+                                      C.byref(loss)))
     return loss.value, grad
 
 

@@ -261,11 +261,12 @@ int ref_gradient_tr(const RefGrid* grid, const RefMedium* medium, const RefSourc
     });
 }
 
-// compute_gradient (gradient.hpp:333-464), time-reversal method, c0, with the dispersion
-// switch of GradientOptions (adjoint and replay steppers, gradient.hpp:22-32,381-384,424-431)
+// compute_gradient (gradient.hpp:333-464), time-reversal method, GradientParam (0 c0, 1 rho0,
+// 2 alpha0, 3 y), with the dispersion switch of GradientOptions (adjoint and replay steppers, gradient.hpp:22-32,381-384,424-431)
 int ref_gradient_tr_opts(const RefGrid* grid, const RefMedium* medium, const RefSources* sources,
                          size_t n_sensors, const size_t* sensor_pos, const double* observed,
-                         int boundary_thickness, int dispersion_enabled, double* grad_out, double* loss_out) {
+                         int boundary_thickness, int dispersion_enabled, int param, double* grad_out,
+                         double* loss_out) {
     return guarded([&] {
         const auto g = to_grid(grid);
         const auto med = to_medium(g, medium);
@@ -279,7 +280,7 @@ int ref_gradient_tr_opts(const RefGrid* grid, const RefMedium* medium, const Ref
         opt.boundary_thickness = boundary_thickness;
         opt.dispersion_enabled = dispersion_enabled != 0;
         const auto res = ustfwi::compute_gradient(med, to_sources(sources), to_sensors(n_sensors, sensor_pos), obs,
-                                                  g, ustfwi::GradientParam::c0, opt);
+                                                  g, static_cast<ustfwi::GradientParam>(param), opt);
         std::memcpy(grad_out, res.grad.data(), g.points() * sizeof(double));
         *loss_out = res.loss;
     });

@@ -25,7 +25,7 @@ EXPORTS = [
     "ustfwi_last_error", "ustfwi_version", "ustfwi_grid_validate", "ustfwi_choose_pml_size",
     "ustfwi_make_grid", "ustfwi_make_pml", "ustfwi_shell_indices", "ustfwi_ball_mask",
     "ustfwi_synth_source_pulse", "ustfwi_draw_realization", "ustfwi_gpu_create", "ustfwi_gpu_destroy",
-    "ustfwi_gpu_set_medium", "ustfwi_gpu_set_gradient_options", "ustfwi_gpu_set_sources", "ustfwi_gpu_set_sensors", "ustfwi_gpu_forward",
+    "ustfwi_gpu_set_medium", "ustfwi_gpu_set_gradient_options", "ustfwi_gpu_set_gradient_param", "ustfwi_gpu_set_sources", "ustfwi_gpu_set_sensors", "ustfwi_gpu_forward",
     "ustfwi_gpu_gradient_tr", "ustfwi_gpu_evaluate_loss", "ustfwi_gpu_derivative",
     "ustfwi_gpu_upload_observed", "ustfwi_gpu_run_gradient", "ustfwi_gpu_download_gradient",
     "ustfwi_gpu_accumulator", "ustfwi_gpu_synchronize", "ustfwi_gpu_stream", "ustfwi_gpu_launch_count",

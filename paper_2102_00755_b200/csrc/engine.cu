@@ -136,11 +136,21 @@ struct ustfwi_gpu_ctx {
     bool grad_dispersion = true;   // GradientOptions::dispersion_enabled (adjoint + replay)
     bool disp_active = false;      // dispersion term of the stepper currently running
     double y_pow = 1.5;
-    float* abs_coef = nullptr;     // tau0, eta, wa1, wa2 (4 fields)
+    float* abs_coef = nullptr;     // tau0, eta (2 fields)
     float* tau0 = nullptr;
     float* eta = nullptr;
-    float* wa1 = nullptr;
-    float* wa2 = nullptr;
+    std::vector<double> alpha0_host;
+    // gradient parameter (GradientParam: 0 c0, 2 alpha0, 3 y) and the accumulator's extra
+    // terms (gradient.hpp:56-142): weight fields wa1, wa2, wa1l, wa2l and the replay rings
+    int grad_param = 0;
+    struct AccPlan {
+        bool ddot = true, a1 = false, a2 = false, a1l = false, a2l = false;
+        bool extra() const { return a1 || a2 || a1l || a2l || !ddot; }
+    } plan;
+    float* acc_mem = nullptr;      // 4 weight fields + 12 ring fields
+    float* wa[4] = {};
+    float* a1lring[3] = {};
+    float* a2lring[3] = {};
     struct AbsScratch {
         float* du[3] = {};
         float* ain = nullptr;
@@ -313,20 +323,18 @@ struct StepIO {
     cudaEvent_t wait_before_z = nullptr;  // cross-stream dependency of the pressure kernel
     // absorbing media
     float abs_sign = 1.f;                 // absorption_sign (-1 in the time-reversal replay)
-    float* a1_out = nullptr;              // replay: |k|^y p and |k|^(y+1) p of the new pressure
-    float* a2_out = nullptr;
 };
 
 // out = F^-1 { |k|^e F{in} } (SpectralEngine::apply_multiplier with power_multiplier(e),
 // engine.hpp:88-94,123-126), through the sim's S1 scratch spectrum.
-void apply_kpow(Ctx& c, Sim& s, const float* in, double e, float* out, cudaStream_t st) {
+void apply_kpow(Ctx& c, Sim& s, const float* in, double e, float* out, cudaStream_t st, int kind = 2) {
     c.count(launch_zfwd(c.g, in, s.S[1], st));
     PencilJobs j{};
     j.buf[0] = s.S[1];
     j.n = 1;
     j.job[0] = {0, 0, nullptr, 0, 0.f};
     c.count(launch_pencil(1, false, c.g, j, st));
-    j.job[0] = {0, 0, nullptr, 2, static_cast<float>(e)};
+    j.job[0] = {0, 0, nullptr, kind, static_cast<float>(e)};
     c.count(launch_pencil(0, false, c.g, j, st));
     j.job[0] = {0, 0, nullptr, 0, 0.f};
     c.count(launch_pencil(1, true, c.g, j, st));
@@ -337,8 +345,7 @@ int sim_index(const Ctx& c, const Sim& s) { return &s == &c.sim[1] ? 1 : 0; }
 
 // Absorbing update_pressure (engine.hpp:327-343) after the density update and the sparse
 // work of the z pass (which left the lossless p in scratch): p = c0^2 (sum rho + s tau aout)
-// - c0^2 eta aout2, then the gathers, the replay's |k|^y / |k|^(y+1) fields, the
-// correlation and the Fy Fz p of the next step.
+// - c0^2 eta aout2, then the gathers and the Fy Fz p of the next step.
 void absorbing_tail(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     auto& sc = c.abs_s[sim_index(c, s)];
     const long long N = c.g.N;
@@ -366,11 +373,6 @@ void absorbing_tail(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     c.count(launch_abs_pressure(N, A, st));
     c.count(launch_gather(io.p_out, io.sens, st));
     c.count(launch_gather(io.p_out, io.shell, st));
-    if (io.a1_out) {
-        apply_kpow(c, s, io.p_out, c.y_pow, io.a1_out, st);
-        if (c.disp_active) apply_kpow(c, s, io.p_out, c.y_pow + 1.0, io.a2_out, st);
-    }
-    if (io.corr.grad) c.count(launch_correlate(N, io.p_out, c.c0sq, io.corr, st));
     c.count(launch_zfwd(c.g, io.p_out, s.S[0], st));
     PencilJobs j{};
     j.buf[0] = s.S[0];
@@ -635,7 +637,111 @@ void forward_sim(Ctx& c, int thickness) {
     if (c.n_sens > 0) c.count(launch_check_finite(c.data, static_cast<long long>(nt) * c.n_sens, c.flags + 2, c.stream));
 }
 
-// compute_gradient, TR branch (gradient.hpp:359-462), GradientParam::c0.
+// GradientAccumulator (gradient.hpp:50-142) for the selected parameter: which terms, their
+// weight fields (fp32, from the fp64 formulas) and the rings of |k|^y-type replay fields.
+void prepare_accumulator(Ctx& c) {
+    const bool disp = c.grad_dispersion && c.y_pow != 2.0;  // dispersion_on_ (gradient.hpp:56)
+    Ctx::AccPlan pl;
+    if (c.grad_param == 0) {
+        pl.a1 = c.absorbing;
+        pl.a2 = c.absorbing && disp;
+    } else if (c.grad_param == 2) {
+        pl.ddot = false;
+        pl.a1 = true;
+        pl.a2 = disp;
+    } else if (c.grad_param == 3) {
+        pl.ddot = false;
+        pl.a1 = pl.a1l = true;
+        pl.a2 = pl.a2l = disp;
+    } else {
+        fail(USTFWI_ERR_INVALID, "the device engine computes the c0, alpha0 and y gradients");
+    }
+    c.plan = pl;
+    if (!pl.extra()) return;
+    const size_t N = static_cast<size_t>(c.g.N);
+    if (!c.acc_mem) {
+        c.acc_mem = c.alloc<float>(16 * N);
+        for (int k = 0; k < 4; ++k) c.wa[k] = c.acc_mem + k * N;
+        for (int r = 0; r < 3; ++r) {
+            c.a1ring[r] = c.acc_mem + (4 + r) * N;
+            c.a2ring[r] = c.acc_mem + (7 + r) * N;
+            c.a1lring[r] = c.acc_mem + (10 + r) * N;
+            c.a2lring[r] = c.acc_mem + (13 + r) * N;
+        }
+    }
+    const double y = c.y_pow;
+    const double tan_term = disp ? std::tan(M_PI * y / 2.0) : 0.0;
+    const double np_of_db = 100.0 * (std::log(10.0) / 20.0) / std::pow(2.0 * M_PI * 1e6, y);  // db2neper(1, y)
+    const double log_conv = std::log(2.0 * M_PI * 1e6);
+    std::vector<float> h(4 * N, 0.f);
+    for (size_t i = 0; i < N; ++i) {
+        const double cc = c.c0_host[i];
+        const double a_np = c.alpha0_host.empty() ? 0.0 : np_of_db * c.alpha0_host[i];
+        double w1 = 0, w2 = 0, w1l = 0, w2l = 0;
+        if (c.grad_param == 0) {  // gradient.hpp:63-73
+            w1 = -2.0 * a_np * (y - 1.0) * std::pow(cc, y - 2.0);
+            w2 = 2.0 * a_np * y * std::pow(cc, y - 1.0) * tan_term;
+        } else if (c.grad_param == 2) {  // :76-88
+            w1 = -2.0 * np_of_db * std::pow(cc, y - 1.0);
+            w2 = 2.0 * np_of_db * std::pow(cc, y) * tan_term;
+        } else {  // :90-116
+            const double tau = -2.0 * a_np * std::pow(cc, y - 1.0);
+            const double lc = std::log(cc) - log_conv;
+            w1 = tau * lc;
+            w1l = 0.5 * tau;
+            if (disp) {
+                const double sec = 1.0 / std::cos(M_PI * y / 2.0);
+                const double eta = 2.0 * a_np * std::pow(cc, y) * tan_term;
+                w2 = eta * lc + M_PI * a_np * std::pow(cc, y) * sec * sec;
+                w2l = 0.5 * eta;
+            }
+        }
+        h[i] = static_cast<float>(w1);
+        h[N + i] = static_cast<float>(w2);
+        h[2 * N + i] = static_cast<float>(w1l);
+        h[3 * N + i] = static_cast<float>(w2l);
+    }
+    CK(cudaMemcpyAsync(c.acc_mem, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+}
+
+// GradientAccumulator::push (gradient.hpp:147-160): the multiplier fields of the newest
+// replay pressure ring[slot].
+void acc_push(Ctx& c, Sim& s, int slot, cudaStream_t st) {
+    if (!c.plan.extra()) return;
+    const float* p = c.ring[slot];
+    if (c.plan.a1) apply_kpow(c, s, p, c.y_pow, c.a1ring[slot], st);
+    if (c.plan.a2) apply_kpow(c, s, p, c.y_pow + 1.0, c.a2ring[slot], st);
+    if (c.plan.a1l) apply_kpow(c, s, p, c.y_pow, c.a1lring[slot], st, 3);
+    if (c.plan.a2l) apply_kpow(c, s, p, c.y_pow + 1.0, c.a2lring[slot], st, 3);
+}
+
+// GradientAccumulator::accumulate (gradient.hpp:166-203) with newer = slot nw, mid, older.
+void acc_correlate(Ctx& c, Correlate cr, int nw, int mid, int old, cudaStream_t st) {
+    cr.use_ddot = c.plan.ddot ? 1 : 0;
+    cr.dt = static_cast<float>(c.grid.dt);
+    if (c.plan.a1) {
+        cr.a1_new = c.a1ring[nw];
+        cr.a1_old = c.a1ring[old];
+        cr.wa1 = c.wa[0];
+    }
+    if (c.plan.a2) {
+        cr.a2_mid = c.a2ring[mid];
+        cr.wa2 = c.wa[1];
+    }
+    if (c.plan.a1l) {
+        cr.a1l_new = c.a1lring[nw];
+        cr.a1l_old = c.a1lring[old];
+        cr.wa1l = c.wa[2];
+    }
+    if (c.plan.a2l) {
+        cr.a2l_mid = c.a2lring[mid];
+        cr.wa2l = c.wa[3];
+    }
+    c.count(launch_correlate(c.g.N, c.ring[nw], c.c0sq, cr, st));
+}
+
+// compute_gradient, TR branch (gradient.hpp:359-462), GradientParam c0 / alpha0 / y.
 void gradient_tr(Ctx& c, int thickness, bool accumulate) {
     require_medium(c);
     if (c.gamma_host.empty()) fail(USTFWI_ERR_INVALID, "gradient computation requires a gamma mask");
@@ -644,6 +750,7 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
     const int nt = c.grid.nt, ns = c.n_sens, last = nt - 1;
     forward_sim(c, thickness);
     c.disp_active = c.dispersion && c.grad_dispersion;  // adjoint + replay steppers (gradient.hpp:381,424-426)
+    prepare_accumulator(c);
     // adjoint source: reverse, Kahan loss, integrate (gradient.hpp:264-289,378-379)
     c.count(launch_adjoint_source(c.data, c.obs, nt, ns, 1, c.q, c.loss_part, c.loss, c.loss + 1,
                                   accumulate ? 1 : 0, c.stream));
@@ -686,10 +793,7 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
         a.diverged = c.flags;
         c.count(launch_zrho(c.g, a, false, sb));
         y_forward_p(c, rep, sb);
-        if (c.absorbing) {  // GradientAccumulator::push of the initial value (gradient.hpp:147-160)
-            apply_kpow(c, rep, c.ring[0], c.y_pow, c.a1ring[0], sb);
-            if (c.disp_active) apply_kpow(c, rep, c.ring[0], c.y_pow + 1.0, c.a2ring[0], sb);
-        }
+        acc_push(c, rep, 0, sb);  // GradientAccumulator::push of the initial value (gradient.hpp:147-160)
     }
     // look-ahead step (gradient.hpp:438-441)
     StepIO rio;
@@ -697,11 +801,8 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
     rio.p_out = c.ring[1];
     rio.check_step = 0;
     rio.abs_sign = -1.f;  // replay stepper: absorption_sign = -1 (gradient.hpp:429-431)
-    if (c.absorbing) {
-        rio.a1_out = c.a1ring[1];
-        rio.a2_out = c.a2ring[1];
-    }
     run_step(c, rep, rio, sb);
+    acc_push(c, rep, 1, sb);
 
     StepIO aio;
     aio.inj = c.adj.view(c.q);
@@ -715,22 +816,18 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
         if (dual) CK(cudaEventRecord(c.ev_adj[n & 1], sa));
         rio.enf.vals = shell_row(last - n - 1);
         rio.p_out = c.ring[(n + 1) % 3];
-        rio.corr = Correlate{c.ring[n % 3], c.ring[(n - 1) % 3], P[n & 1], c.grad, inv_dt};
-        if (c.absorbing) {
-            rio.a1_out = c.a1ring[(n + 1) % 3];
-            rio.a2_out = c.a2ring[(n + 1) % 3];
-            rio.corr.a1_new = c.a1ring[(n + 1) % 3];
-            rio.corr.a1_old = c.a1ring[(n - 1) % 3];
-            rio.corr.wa1 = c.wa1;
-            if (c.disp_active) {
-                rio.corr.a2_mid = c.a2ring[n % 3];
-                rio.corr.wa2 = c.wa2;
-            }
-            rio.corr.dt = static_cast<float>(c.grid.dt);
-        }
+        // plain c0 gradient: the correlation runs inside the replay's pressure kernel;
+        // otherwise (absorption terms, alpha0 / y) after the step, from the rings
+        const Correlate corr{c.ring[n % 3], c.ring[(n - 1) % 3], P[n & 1], c.grad, inv_dt};
+        const bool fused = !c.plan.extra() && !c.absorbing;
+        rio.corr = fused ? corr : Correlate{};
         rio.check_step = ((n + 1) & 63) == 0 ? n + 1 : 0;
         rio.wait_before_z = dual ? c.ev_adj[n & 1] : nullptr;                 // adjoint step n done
         run_step(c, rep, rio, sb);
+        if (!fused) {
+            acc_push(c, rep, (n + 1) % 3, sb);
+            acc_correlate(c, corr, (n + 1) % 3, n % 3, (n - 1) % 3, sb);
+        }
         if (dual) CK(cudaEventRecord(c.ev_rep[n & 1], sb));
     }
     if (dual) {
@@ -752,7 +849,7 @@ void set_absorption(Ctx& c, const double* alpha0, double y, const double* c0) {
     c.dispersion = c.absorbing && y != 2.0;
     if (!c.absorbing) return;
     const size_t N = static_cast<size_t>(c.g.N);
-    std::vector<float> h(4 * N);
+    std::vector<float> h(2 * N);
     const double tan_term = c.dispersion ? std::tan(M_PI * y / 2.0) : 0.0;
     const double np_per_db = 100.0 * (std::log(10.0) / 20.0) / std::pow(2.0 * M_PI * 1e6, y);  // db2neper
     for (size_t i = 0; i < N; ++i) {
@@ -760,17 +857,13 @@ void set_absorption(Ctx& c, const double* alpha0, double y, const double* c0) {
         const double cc = c0[i];
         h[i] = static_cast<float>(-2.0 * a * std::pow(cc, y - 1.0));
         h[N + i] = static_cast<float>(2.0 * a * std::pow(cc, y) * tan_term);
-        h[2 * N + i] = static_cast<float>(-2.0 * a * (y - 1.0) * std::pow(cc, y - 2.0));
-        h[3 * N + i] = static_cast<float>(2.0 * a * y * std::pow(cc, y - 1.0) * tan_term);
     }
-    c.abs_coef = c.alloc<float>(4 * N);
+    c.abs_coef = c.alloc<float>(2 * N);
     CK(cudaMemcpyAsync(c.abs_coef, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice, c.stream));
     c.tau0 = c.abs_coef;
     c.eta = c.abs_coef + N;
-    c.wa1 = c.abs_coef + 2 * N;
-    c.wa2 = c.abs_coef + 3 * N;
-    // per stepper: du x3, ain, aout, aout2, sum; replay rings a1 x3, a2 x3
-    c.abs_mem = c.alloc<float>(20 * N);
+    // per stepper: du x3, ain, aout, aout2, sum
+    c.abs_mem = c.alloc<float>(14 * N);
     float* m = c.abs_mem;
     for (int k = 0; k < 2; ++k) {
         auto& sc = c.abs_s[k];
@@ -780,11 +873,7 @@ void set_absorption(Ctx& c, const double* alpha0, double y, const double* c0) {
         sc.aout2 = m + (k * 7 + 5) * N;
         sc.sum = m + (k * 7 + 6) * N;
     }
-    for (int r = 0; r < 3; ++r) {
-        c.a1ring[r] = m + (14 + r) * N;
-        c.a2ring[r] = m + (17 + r) * N;
-    }
-    CK(cudaMemsetAsync(c.abs_mem, 0, 20 * N * sizeof(float), c.stream));
+    CK(cudaMemsetAsync(c.abs_mem, 0, 14 * N * sizeof(float), c.stream));
 }
 
 template <class Fn>
@@ -1068,6 +1157,8 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
             }
         }
         set_absorption(*c, absorbing ? alpha0 : nullptr, y, c0);
+        if (alpha0) c->alpha0_host.assign(alpha0, alpha0 + N);
+        else c->alpha0_host.clear();
         c->gamma_host.clear();
         if (gamma) {
             c->gamma_host.assign(gamma, gamma + N);
@@ -1082,6 +1173,15 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
 
 int ustfwi_gpu_set_gradient_options(ustfwi_gpu_ctx* c, int dispersion_enabled) {
     return guarded(c, [&] { c->grad_dispersion = dispersion_enabled != 0; });
+}
+
+int ustfwi_gpu_set_gradient_param(ustfwi_gpu_ctx* c, int param) {
+    return guarded(c, [&] {
+        if (param == 1)
+            fail(USTFWI_ERR_INVALID, "the rho0 gradient is not provided (defective in the reference, SURVEY F3)");
+        if (param != 0 && param != 2 && param != 3) fail(USTFWI_ERR_INVALID, "unknown gradient parameter");
+        c->grad_param = param;
+    });
 }
 
 int ustfwi_gpu_set_sources(ustfwi_gpu_ctx* c, size_t n_src, const size_t* pos, const size_t* sig_off,

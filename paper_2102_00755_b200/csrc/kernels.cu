@@ -53,14 +53,15 @@ __global__ void __launch_bounds__(256) pencil_pass_kernel(GridDev g, PencilJobs 
         // kappa (or |k|^e) for the tile: k = (kx[j], ky[y], kz[c0 + c]); one multiplier kind
         // per launch
         const float ky = g.ky[blockIdx.y];
-        const bool power = jobs.job[0].kappa == 2;
+        const int kind = jobs.job[0].kappa;
+        const bool power = kind >= 2;
         const float e = jobs.job[0].kexp;
         for (int t = threadIdx.x; t < n_el; t += blockDim.x) {
             const int j = t / TB, c = t % TB;
             const float kx = g.kx[j];
             const float kz = (c < ncol) ? g.kz[c0 + c] : 0.f;
             const float k2 = kx * kx + ky * ky + kz * kz;
-            kap[t] = power ? kpow_mult(k2, e) : kappa_of(k2, g.half_cdt);
+            kap[t] = power ? kpow_mult(k2, e, kind) : kappa_of(k2, g.half_cdt);
         }
     }
 
@@ -472,9 +473,11 @@ __global__ void correlate_kernel(long long n, const float* __restrict__ p_new, c
         const float q = C.q_adj[i];
         const float w = 2.f / (c2 * sqrtf(c2));
         float gv = C.grad[i];
-        gv += w * (((p_new[i] - 2.f * C.p_mid[i]) + C.p_old[i]) * C.inv_dt) * q;
+        if (C.use_ddot) gv += w * (((p_new[i] - 2.f * C.p_mid[i]) + C.p_old[i]) * C.inv_dt) * q;
         if (C.a1_new) gv += C.wa1[i] * (0.5f * (C.a1_old[i] - C.a1_new[i])) * q;
+        if (C.a1l_new) gv += C.wa1l[i] * (0.5f * (C.a1l_old[i] - C.a1l_new[i])) * q;
         if (C.a2_mid) gv += C.wa2[i] * C.a2_mid[i] * q * C.dt;
+        if (C.a2l_mid) gv += C.wa2l[i] * C.a2l_mid[i] * q * C.dt;
         C.grad[i] = gv;
     }
 }

@@ -69,13 +69,21 @@ struct Correlate {
     const float* q_adj;
     float* grad;
     float inv_dt;
-    // absorbing media (gradient.hpp:63-74,183-203): grad += wa1 * (a1_old - a1_new)/2 * q
-    // + wa2 * a2_mid * q * dt with a1 = |k|^y p, a2 = |k|^(y+1) p of the replay pressures
+    // GradientAccumulator::accumulate (gradient.hpp:177-203) beyond the c0 ddot term (used by
+    // the stand-alone correlate kernel only): grad += wa1 (a1_old - a1_new)/2 q
+    // + wa1l (a1l_old - a1l_new)/2 q + wa2 a2_mid q dt + wa2l a2l_mid q dt with a1 = |k|^y p,
+    // a2 = |k|^(y+1) p, a1l / a2l the same times log|k|^2, of the replay pressures
+    int use_ddot = 1;
     const float* a1_new = nullptr;
     const float* a1_old = nullptr;
     const float* a2_mid = nullptr;
+    const float* a1l_new = nullptr;
+    const float* a1l_old = nullptr;
+    const float* a2l_mid = nullptr;
     const float* wa1 = nullptr;
     const float* wa2 = nullptr;
+    const float* wa1l = nullptr;
+    const float* wa2l = nullptr;
     float dt = 0.f;
 };
 
@@ -97,15 +105,19 @@ struct PencilJob {
     int src;              // scratch buffer index read
     int dst;              // scratch buffer index written
     const float2* dmul;   // per-index factor along the pass axis (D_a table), nullable
-    int kappa;            // X pass only: 1 multiply by kappa(|k|), 2 by |k|^kexp (power_multiplier)
-    float kexp;           // exponent of |k| for kappa == 2 (engine.hpp:88-94)
+    int kappa;            // X pass only: 1 multiply by kappa(|k|), 2 by |k|^kexp (power_multiplier),
+                          // 3 by |k|^kexp log|k|^2
+    float kexp;           // exponent of |k| for kappa == 2, 3 (engine.hpp:88-101)
 };
 
 // power_multiplier (engine.hpp:88-94): |k|^e over the half spectrum, the k = 0 bin 1 for
-// e == 0 and 0 otherwise (fractional-Laplacian convention)
-__device__ __forceinline__ float kpow_mult(float k2, float e) {
-    if (k2 == 0.f) return e == 0.f ? 1.f : 0.f;
-    return powf(k2, 0.5f * e);
+// e == 0 and 0 otherwise (fractional-Laplacian convention); kind 3: times log_k2_multiplier
+// (engine.hpp:97-101, 0 at k = 0), as GradientAccumulator builds mult_a1l / mult_a2l
+// (gradient.hpp:132-142)
+__device__ __forceinline__ float kpow_mult(float k2, float e, int kind = 2) {
+    if (k2 == 0.f) return (kind == 2 && e == 0.f) ? 1.f : 0.f;
+    const float m = powf(k2, 0.5f * e);
+    return kind == 3 ? m * logf(k2) : m;
 }
 
 struct PencilJobs {

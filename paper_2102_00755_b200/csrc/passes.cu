@@ -240,14 +240,15 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
                         // kappa(|k|) (or |k|^e) of this tile, evaluated once for all its source groups
                         const float ky = g.ky[w.line];
                         const float kz = colok ? g.kz[w.c0 + c] : 0.f;
-                        const bool power = jobs.job[gstart[w.grp]].kappa == 2;
+                        const int kind = jobs.job[gstart[w.grp]].kappa;
+                        const bool power = kind >= 2;
                         const float e = jobs.job[gstart[w.grp]].kexp;
 #pragma unroll
                         for (int k2 = 0; k2 < N2; ++k2) {
                             const int k = C::out_row(kb, k2);
                             const float kx = g.kx[k];
                             const float q2 = kx * kx + ky * ky + kz * kz;
-                            kap_s[k * TB + c] = power ? kpow_mult(q2, e) : kappa_fast(q2, g.half_cdt);
+                            kap_s[k * TB + c] = power ? kpow_mult(q2, e, kind) : kappa_fast(q2, g.half_cdt);
                         }
                     }
 #pragma unroll
@@ -439,14 +440,15 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
                     if (grp == 0) {
                         const float ky = g.ky[line];
                         const float kz = col0 + c < g.nzh ? g.kz[col0 + c] : 0.f;
-                        const bool power = jobs.job[gb].kappa == 2;  // one multiplier kind per launch
+                        const int kind = jobs.job[gb].kappa;  // one multiplier kind per launch
+                        const bool power = kind >= 2;
                         const float e = jobs.job[gb].kexp;
 #pragma unroll
                         for (int k2 = 0; k2 < N2; ++k2) {
                             const int k = C::out_row(kb, k2);
                             const float kx = g.kx[k];
                             const float q2 = kx * kx + ky * ky + kz * kz;
-                            kap_s[k * TB + c] = power ? kpow_mult(q2, e) : kappa_fast(q2, g.half_cdt);
+                            kap_s[k * TB + c] = power ? kpow_mult(q2, e, kind) : kappa_fast(q2, g.half_cdt);
                         }
                     }
 #pragma unroll

@@ -190,13 +190,20 @@ class GpuEngine:
                                                  C.byref(loss)))
         return loss.value, grad
 
-    def gradient_tr(self, observed: np.ndarray, thickness: int, dispersion_enabled: bool = True):
+    PARAMS = {"c0": 0, "rho0": 1, "alpha0": 2, "y": 3}
+
+    def gradient_tr(self, observed: np.ndarray, thickness: int, dispersion_enabled: bool = True,
+                    param: str = "c0"):
         """-> (loss, grad) ; grad zero outside gamma. dispersion_enabled: GradientOptions
-        (gradient.hpp:31), the adjoint / replay dispersion term of absorbing media."""
+        (gradient.hpp:31), the adjoint / replay dispersion term of absorbing media; param:
+        GradientParam c0 | alpha0 | y (gradient.hpp:9; rho0 is rejected)."""
         obs = np.ascontiguousarray(observed, dtype=np.float64)
         if obs.shape != (self.n_sensors, self.grid.nt):
             raise ValueError("observed data dimensions do not match the simulation")
+        if param not in self.PARAMS:
+            raise ValueError("unknown gradient parameter")
         check(lib().ustfwi_gpu_set_gradient_options(self._h, int(bool(dispersion_enabled))))
+        check(lib().ustfwi_gpu_set_gradient_param(self._h, self.PARAMS[param]))
         grad = np.zeros(self.grid.shape)
         loss = C.c_double(0.0)
         check(lib().ustfwi_gpu_gradient_tr(self._h, ptr(obs, C.c_double), int(thickness), ptr(grad, C.c_double),

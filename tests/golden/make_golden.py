@@ -13,8 +13,9 @@ Fixtures (small, committed):
   config_a_short.npz  config A truncated to nt=96 with f_obs = 0 (fast GPU parity case)
   config_a_absorb.npz config A at nt=96 with power-law absorption (alpha0 3 dB/(MHz^y cm) in
                       gamma, 0.5 outside): y = 1.5 traces + TR gradient + loss (f_obs = 0), the
-                      same gradient with GradientOptions::dispersion_enabled = false, y = 2 (no
-                      dispersion term) traces
+                      same gradient with GradientOptions::dispersion_enabled = false, the alpha0
+                      and y gradients (GradientParam), the alpha0 gradient of the lossless model,
+                      y = 2 (no dispersion term) traces
 """
 from __future__ import annotations
 
@@ -121,8 +122,14 @@ def config_a_absorb_fixture(nt=96):
     loss, grad = ref.gradient_time_reversal(g, m15, pos, sig, sc.sensors.positions, observed, 8)
     loss_nd, grad_nd = ref.gradient_tr_opts(g, m15, pos, sig, sc.sensors.positions, observed, 8,
                                             dispersion_enabled=False)
+    loss_a0, grad_a0 = ref.gradient_tr_opts(g, m15, pos, sig, sc.sensors.positions, observed, 8, param="alpha0")
+    loss_y, grad_y = ref.gradient_tr_opts(g, m15, pos, sig, sc.sensors.positions, observed, 8, param="y")
+    _, grad_a0_lossless = ref.gradient_tr_opts(g, sc.model, pos, sig, sc.sensors.positions, observed, 8,
+                                               param="alpha0")
     gidx = np.flatnonzero(np.asarray(sc.model.gamma).ravel())
-    np.savez_compressed(os.path.join(OUT, "config_a_absorb.npz"), nt=g.nt, data_y15=data15, data_y20=data20,
+    extra = dict(grad_alpha0=grad_a0.ravel()[gidx], grad_y=grad_y.ravel()[gidx],
+                 grad_alpha0_lossless=grad_a0_lossless.ravel()[gidx], loss_alpha0=loss_a0, loss_y=loss_y)
+    np.savez_compressed(os.path.join(OUT, "config_a_absorb.npz"), **extra, nt=g.nt, data_y15=data15, data_y20=data20,
                         data_lossless=lossless, trace_checksum=np.array([trace.sum(), np.abs(trace).sum()]),
                         loss=loss, grad_gamma=grad.ravel()[gidx], gamma_idx=gidx,
                         loss_nodisp=loss_nd, grad_gamma_nodisp=grad_nd.ravel()[gidx])

@@ -88,3 +88,25 @@ def test_lossless_after_absorbing_medium(setup, golden):
     eng.set_medium(sc.model)
     data, _ = eng.forward(0)
     assert rel(data, z["data_lossless"]) < TRACE_TOL
+
+
+@pytest.mark.parametrize("param,key,lossless", [("alpha0", "grad_alpha0", False), ("y", "grad_y", False),
+                                                ("alpha0", "grad_alpha0_lossless", True)])
+def test_alpha0_and_y_gradients(setup, param, key, lossless):
+    # GradientParam alpha0 / y (gradient.hpp:76-116): no c0 ddot term, |k|^y and |k|^(y+1)
+    # (times log|k|^2 for y) fields of the replay pressures; the alpha0 weights do not depend
+    # on alpha0, so the lossless model has a non-zero alpha0 gradient too
+    sc, z, eng = setup
+    eng.set_medium(sc.model if lossless else absorbing(sc.model, 1.5))
+    observed = np.zeros((len(sc.sensors.positions), int(z["nt"])))
+    loss, grad = eng.gradient_tr(observed, 8, param=param)
+    if not lossless:
+        assert abs(loss - float(z["loss_" + param])) <= 1e-4 * abs(float(z["loss_" + param]))
+    assert rel(grad.ravel()[z["gamma_idx"]], z[key]) < GRAD_TOL
+
+
+def test_rho0_gradient_is_rejected(setup):
+    sc, z, eng = setup
+    eng.set_medium(sc.model)
+    with pytest.raises(ValueError, match="rho0"):
+        eng.gradient_tr(np.zeros((len(sc.sensors.positions), int(z["nt"]))), 8, param="rho0")
