@@ -52,6 +52,10 @@ __device__ __forceinline__ float kappa_fast(float k2, float half_cdt) {
     return fmaf(-s, u, 1.f);
 }
 
+// |k|^e multipliers of the absorbing / alpha0 / y paths, kept out of line so the hot x-pass
+// code (kappa) stays compact
+__device__ __noinline__ float kpow_mult_call(float k2, float e, int kind) { return kpow_mult(k2, e, kind); }
+
 // ======================================================================================
 // Pencil passes (x and y)
 // ======================================================================================
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
                             const int k = C::out_row(kb, k2);
                             const float kx = g.kx[k];
                             const float q2 = kx * kx + ky * ky + kz * kz;
-                            kap_s[k * TB + c] = power ? kpow_mult(q2, e, kind) : kappa_fast(q2, g.half_cdt);
+                            kap_s[k * TB + c] = power ? kpow_mult_call(q2, e, kind) : kappa_fast(q2, g.half_cdt);
                         }
                     }
 #pragma unroll
@@ -448,7 +452,7 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
                             const int k = C::out_row(kb, k2);
                             const float kx = g.kx[k];
                             const float q2 = kx * kx + ky * ky + kz * kz;
-                            kap_s[k * TB + c] = power ? kpow_mult(q2, e, kind) : kappa_fast(q2, g.half_cdt);
+                            kap_s[k * TB + c] = power ? kpow_mult_call(q2, e, kind) : kappa_fast(q2, g.half_cdt);
                         }
                     }
 #pragma unroll
