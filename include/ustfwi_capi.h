@@ -216,6 +216,21 @@ USTFWI_API int ustfwi_lbfgs_apply(ustfwi_lbfgs* h, const double* g, double* out)
 /* Number of stored pairs and the current H0 scaling. */
 USTFWI_API int ustfwi_lbfgs_pairs(const ustfwi_lbfgs* h, int* count, double* gamma);
 
+/* ---- multigrid transfer on the device (§3.3, Appendix C) ----
+ * fourier_interpolate (grid/spectral.hpp:166-212): field [dims] -> out [new_dims], every
+ * target dim even and >= 4, every source dim even; blackman != 0 applies the separable
+ * Blackman taper (prolong_model). Host fp64 buffers. */
+USTFWI_API int ustfwi_fourier_interpolate(int device, int ndim, const int* dims, const double* field,
+                                          const int* new_dims, int blackman, double* out);
+/* lowpass_filter_timeseries (grid/filter.hpp:88-101) of n_series rows of len samples. */
+USTFWI_API int ustfwi_lowpass_timeseries(int device, size_t n_series, size_t len, const double* sig, double dt,
+                                         double cutoff_hz, double transition, double atten_db, double* out);
+/* restrict_data: [n_series][nt] -> [n_series][ceil(nt/eta)], Fourier
+ * resampling, Kaiser low-pass (transition 0.1, 60 dB) at cutoff_hz, scale eta^(ndim-1).
+ * out == NULL: only *nt_out is set. */
+USTFWI_API int ustfwi_restrict_traces(int device, size_t n_series, size_t nt, const double* data, int eta, int ndim,
+                                      double dt_fine, double cutoff_hz, double* out, size_t* nt_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -299,3 +299,24 @@ def time_steps(g, medium, k_fwd, k_pair):
     b = C.c_double(0)
     _check(lib().ref_time_steps(C.byref(s), C.byref(m), k_fwd, k_pair, C.byref(a), C.byref(b)))
     return a.value, b.value
+
+
+def fourier_interpolate(f, new_dims, blackman=False):
+    """fourier_interpolate (spectral.hpp:166-212)."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    nd = len(f.shape)
+    dims = (C.c_int * nd)(*f.shape)
+    ndims = (C.c_int * nd)(*new_dims)
+    out = np.zeros(tuple(new_dims))
+    _check(lib().ref_fourier_interpolate(nd, dims, _p(f, C.c_double), ndims, int(bool(blackman)),
+                                         _p(out, C.c_double)))
+    return out
+
+
+def lowpass_timeseries(sig, dt, cutoff_hz, transition=0.1, atten_db=60.0):
+    """lowpass_filter_timeseries (filter.hpp:88-101)."""
+    x = np.ascontiguousarray(sig, dtype=np.float64)
+    out = np.zeros_like(x)
+    _check(lib().ref_lowpass_timeseries(_p(x, C.c_double), C.c_size_t(x.size), C.c_double(dt), C.c_double(cutoff_hz),
+                                        C.c_double(transition), C.c_double(atten_db), _p(out, C.c_double)))
+    return out

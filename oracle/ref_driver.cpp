@@ -17,6 +17,7 @@
 #include <string>
 
 #include "ustfwi/adjoint/gradient.hpp"
+#include "ustfwi/grid/filter.hpp"
 
 extern "C" {
 
@@ -185,6 +186,29 @@ int ref_spectral_derivative(const RefGrid* grid, const double* f, int axis, int 
         std::memcpy(in.data(), f, g.points() * sizeof(double));
         const auto o = ustfwi::spectral_derivative(in, axis, static_cast<ustfwi::Stagger>(stagger), kv);
         std::memcpy(out, o.data(), g.points() * sizeof(double));
+    });
+}
+
+// fourier_interpolate (spectral.hpp:166-212)
+int ref_fourier_interpolate(int ndim, const int* dims, const double* f, const int* new_dims, int blackman,
+                            double* out) {
+    return guarded([&] {
+        ustfwi::Dims d(dims, dims + ndim), nd(new_dims, new_dims + ndim);
+        ustfwi::Field in(d);
+        std::memcpy(in.data(), f, in.size() * sizeof(double));
+        const auto o = ustfwi::fourier_interpolate(in, nd, blackman ? ustfwi::SpectralWindow::blackman
+                                                                    : ustfwi::SpectralWindow::none);
+        std::memcpy(out, o.data(), o.size() * sizeof(double));
+    });
+}
+
+// lowpass_filter_timeseries (filter.hpp:88-101)
+int ref_lowpass_timeseries(const double* sig, size_t len, double dt, double cutoff_hz, double transition,
+                           double atten_db, double* out) {
+    return guarded([&] {
+        std::vector<double> x(sig, sig + len);
+        const auto o = ustfwi::lowpass_filter_timeseries(x, dt, cutoff_hz, transition, atten_db);
+        std::memcpy(out, o.data(), o.size() * sizeof(double));
     });
 }
 

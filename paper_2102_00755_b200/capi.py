@@ -31,7 +31,7 @@ EXPORTS = [
     "ustfwi_gpu_accumulator", "ustfwi_gpu_synchronize", "ustfwi_gpu_stream", "ustfwi_gpu_launch_count",
     "ustfwi_gpu_shell_size", "ustfwi_gpu_set_profiling", "ustfwi_gpu_kernel_stats", "ustfwi_nccl_unique_id", "ustfwi_gpu_comm_init", "ustfwi_gpu_allreduce_mean",
     "ustfwi_lbfgs_create", "ustfwi_lbfgs_destroy", "ustfwi_lbfgs_reset", "ustfwi_lbfgs_push", "ustfwi_lbfgs_apply",
-    "ustfwi_lbfgs_pairs",
+    "ustfwi_lbfgs_pairs", "ustfwi_fourier_interpolate", "ustfwi_lowpass_timeseries", "ustfwi_restrict_traces",
 ]
 
 

@@ -11,6 +11,8 @@ Fixtures (small, committed):
   config_a.npz        config A (64^3, nt=393): observed data (truth medium), model traces,
                       subsampled shell trace, TR gradient on gamma and loss
   config_a_short.npz  config A truncated to nt=96 with f_obs = 0 (fast GPU parity case)
+  multigrid.npz       fourier_interpolate (up / down / mixed, with and without the Blackman
+                      taper, 3-D and 2-D) and lowpass_filter_timeseries on seeded inputs
   config_a_absorb.npz config A at nt=96 with power-law absorption (alpha0 3 dB/(MHz^y cm) in
                       gamma, 0.5 outside): y = 1.5 traces + TR gradient + loss (f_obs = 0), the
                       same gradient with GradientOptions::dispersion_enabled = false, the alpha0
@@ -100,6 +102,24 @@ def config_a_fixture(nt, name, trace_stride=(8, 16), observed_zero=False):
     print(f"{name}: fwd {t1 - t0:.1f}s fwd+trace {t2 - t1:.1f}s gradient {t3 - t2:.1f}s loss {loss:.6e}")
 
 
+def multigrid_fixture():
+    rng = np.random.default_rng(23)
+    out = {}
+    cases = {"up": ((12, 10, 8), (16, 20, 12)), "down": ((16, 20, 12), (8, 10, 6)), "mixed": ((12, 10, 8), (8, 20, 8)),
+             "2d": ((32, 24), (48, 16))}
+    for name, (src, dst) in cases.items():
+        f = rng.standard_normal(src)
+        out[f"{name}_in"] = f
+        out[f"{name}_dims"] = np.array(dst)
+        out[f"{name}_none"] = ref.fourier_interpolate(f, dst, False)
+        out[f"{name}_blackman"] = ref.fourier_interpolate(f, dst, True)
+    sig = rng.standard_normal((4, 500))
+    out["lp_in"] = sig
+    out["lp_1MHz"] = np.stack([ref.lowpass_timeseries(x, 1e-7, 1e6) for x in sig])
+    out["lp_2MHz_tr02_a40"] = np.stack([ref.lowpass_timeseries(x, 1e-7, 2e6, 0.2, 40.0) for x in sig])
+    np.savez_compressed(os.path.join(OUT, "multigrid.npz"), **out)
+
+
 def absorbing_medium(m, y):
     import copy
     a = copy.copy(m)
@@ -138,6 +158,9 @@ def config_a_absorb_fixture(nt=96):
 
 
 if __name__ == "__main__":
+    if "--multigrid-only" in sys.argv:
+        multigrid_fixture()
+        sys.exit(0)
     if "--absorb-only" in sys.argv:
         config_a_absorb_fixture()
         sys.exit(0)
@@ -146,6 +169,7 @@ if __name__ == "__main__":
     derivative_fixture()
     forward_2d_fixture()
     config_a_fixture(96, "config_a_short", observed_zero=True)
+    multigrid_fixture()
     config_a_absorb_fixture()
     if "--quick" not in sys.argv:
         config_a_fixture(None, "config_a")
