@@ -1452,10 +1452,19 @@ cudaError_t launch_pencil_fast(int axis, bool inv, const GridDev& g, const Penci
         case 144: return pencil_sized<144, 16, 16, 3, false>(axis, inv, g, j, st);
         case 256: return pencil_sized<256, 16, 16, 3, false>(axis, inv, g, j, st);
         case 480:
-            // measured on B200 (config D): prime-factor 32x15 is fastest for the x pass (no
-            // inter-level twiddles), Cooley-Tukey 30x16 for the y pass; both double-buffered
-            return axis == 0 ? pencil_sized<480, 32, 8, 2, true>(axis, inv, g, j, st)
-                             : pencil_sized<480, 30, 8, 2, true>(axis, inv, g, j, st);
+            // measured on B200 (config D): Cooley-Tukey 30x16 for both passes (double-buffered
+            // TMA tiles)
+            if (axis == 0) {
+                // USTFWI_X480=1: prime-factor 32x15 (spills at the 128-register cap with TMA
+                // tiles; 0.352 vs 0.312 ms per launch at config D)
+                static const int xv = [] {
+                    const char* e = std::getenv("USTFWI_X480");
+                    return e ? std::atoi(e) : 0;
+                }();
+                if (xv == 1) return pencil_sized<480, 32, 8, 2, true>(axis, inv, g, j, st);
+                return pencil_sized<480, 30, 8, 2, true>(axis, inv, g, j, st);
+            }
+            return pencil_sized<480, 30, 8, 2, true>(axis, inv, g, j, st);
         default: return cudaErrorInvalidValue;
     }
 }
