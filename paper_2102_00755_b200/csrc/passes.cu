@@ -1542,7 +1542,10 @@ cudaError_t zvel_sized(const GridDev& g, float2* S[3], const float2* dz_plus, fl
     }
     a.dz_plus = dz_plus;
     a.pml = pml;
-    if (use_zrow2()) return zvel2_sized<M>(g, a, st);
+    // paired-residue rows where they win on B200: z-vel for M >= 64 (config B 0.036 -> 0.027 ms,
+    // D 0.80 -> 0.54 ms), the density/pressure pair for M >= 128 only (config A/B: the
+    // 8-row kernels are faster, 0.037 vs 0.062 ms at A)
+    if (M >= 64 && use_zrow2()) return zvel2_sized<M>(g, a, st);
     const size_t smem = C::FIXED + size_t(kZRows) * g.nzp * 8 + size_t(r[0].field ? 2 : 1) * kZRows * C::NZ * 4;
     auto kern = zvel_fast_kernel<M, N1, kZRows>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1558,7 +1561,7 @@ cudaError_t zrho_sized(const GridDev& g, const ZrhoArgs& za, cudaStream_t st) {
     a.a = za;
     const unsigned blocks = (unsigned)(((long long)g.xn * g.ny + kZRows - 1) / kZRows);
     // density update, one CTA per (row block, axis)
-    if (use_zrow2()) return zrho2_sized<M>(g, a, st);
+    if (M >= 128 && use_zrow2()) return zrho2_sized<M>(g, a, st);
     {
     const size_t smem1 = 16 + size_t(M) * 8 + size_t(kZRows) * C::ZT * 8 + size_t(kZRows) * g.nzp * 8 +
                          size_t(za.dtrho0.field ? 2 : 1) * kZRows * C::NZ * 4;
