@@ -53,6 +53,7 @@ struct InjectSet {
     float* w = nullptr;
     float* sig = nullptr;              // owned signal table (sources) or borrowed (adjoint q)
     float* scale = nullptr;
+    int* blk8 = nullptr;               // per 8-row block offsets into pos
     SparseInject view(const float* sig_override = nullptr) const {
         SparseInject s;
         s.n_unique = n_unique;
@@ -65,6 +66,7 @@ struct InjectSet {
         s.w = w;
         s.sig = sig_override ? sig_override : sig;
         s.scale = scale;
+        s.blk8 = blk8;
         return s;
     }
 };
@@ -174,6 +176,7 @@ struct ustfwi_gpu_ctx {
     std::vector<size_t> sens_pos_host;
     int* sens_pos = nullptr;   // sorted
     int* sens_idx = nullptr;
+    int* sens_blk8 = nullptr;
     float* data = nullptr;     // [nt][ns]
     double* obs = nullptr;     // [nt][ns]
     float* q = nullptr;        // [nt][ns]
@@ -184,6 +187,7 @@ struct ustfwi_gpu_ctx {
     int shell_thickness = 0;
     std::vector<size_t> shell_host;
     int* shell_pos = nullptr;
+    int* shell_blk8 = nullptr;
     float* trace = nullptr;
     size_t trace_elems = 0;
 
@@ -514,12 +518,27 @@ void y_forward_p(Ctx& c, Sim& s, cudaStream_t st) {
     c.count(launch_pencil(1, false, c.g, j, st));
 }
 
+// blk8[b] = index of the first sorted position >= b * 8 rows (b = 0 .. ceil(rows/8)): the
+// sparse work of an 8-row-aligned row block is found with two loads instead of a search
+int* upload_blk8(Ctx& c, const std::vector<int>& sorted_pos) {
+    const long long rows = c.g.rows, nz = c.g.nz;
+    const long long nb = (rows + 7) / 8;
+    std::vector<int> off(static_cast<size_t>(nb + 1));
+    size_t k = 0;
+    for (long long b = 0; b <= nb; ++b) {
+        const long long key = b * 8 * nz;
+        while (k < sorted_pos.size() && sorted_pos[k] < key) ++k;
+        off[static_cast<size_t>(b)] = static_cast<int>(k);
+    }
+    return c.upload(off);
+}
+
 // Build the device InjectSet for `n` contributions at flat positions pos[i].
 void build_inject(Ctx& c, InjectSet& set, const std::vector<size_t>& pos, const std::vector<int>& off,
                   const std::vector<int>& len, const std::vector<int>& stride, const std::vector<int>& delay,
                   const std::vector<float>& w) {
     for (void* p : {(void*)set.pos, (void*)set.csr, (void*)set.off, (void*)set.len, (void*)set.stride,
-                    (void*)set.delay, (void*)set.w, (void*)set.scale})
+                    (void*)set.delay, (void*)set.w, (void*)set.scale, (void*)set.blk8})
         c.release(p);
     const size_t n = pos.size();
     std::vector<size_t> order(n);
@@ -550,6 +569,7 @@ void build_inject(Ctx& c, InjectSet& set, const std::vector<size_t>& pos, const 
     set.delay = c.upload(d);
     set.w = c.upload(ww);
     set.scale = c.alloc<float>(upos.size());
+    set.blk8 = upload_blk8(c, upos);
 }
 
 // inject_mass_source scale 2*dt/(ndim*dx*c0(x)) (engine.hpp:296-300), from the current medium.
@@ -585,6 +605,8 @@ void prepare_shell(Ctx& c, int thickness) {
         c.shell_host = ustfwi_host::shell_indices(c.gamma_host, dims, thickness);
         std::vector<int> sp(c.shell_host.begin(), c.shell_host.end());
         c.shell_pos = c.upload(sp);
+        c.release(c.shell_blk8);
+        c.shell_blk8 = upload_blk8(c, sp);
         c.shell_thickness = thickness;
     }
     const size_t need = c.shell_host.size() * static_cast<size_t>(c.grid.nt);
@@ -624,8 +646,8 @@ void forward_sim(Ctx& c, int thickness) {
     const int n_shell = thickness > 0 ? static_cast<int>(c.shell_host.size()) : 0;
     StepIO io;
     io.inj = c.src.view();
-    io.sens = SparseGather{c.n_sens, c.sens_pos, c.sens_idx, nullptr};
-    io.shell = SparseGather{n_shell, c.shell_pos, nullptr, nullptr};
+    io.sens = SparseGather{c.n_sens, c.sens_pos, c.sens_idx, nullptr, c.sens_blk8};
+    io.shell = SparseGather{n_shell, c.shell_pos, nullptr, nullptr, c.shell_blk8};
     io.p_out = s.p;
     for (int n = 0; n < nt; ++n) {
         io.step_n = n;
@@ -789,7 +811,7 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
         a.c0sq = c.c0sq;
         a.p_out = c.ring[0];
         a.a_first = c.off_axis;
-        a.enf = SparseEnforce{n_shell, c.shell_pos, shell_row(last), static_cast<float>(c.ndim)};
+        a.enf = SparseEnforce{n_shell, c.shell_pos, shell_row(last), static_cast<float>(c.ndim), c.shell_blk8};
         a.diverged = c.flags;
         c.count(launch_zrho(c.g, a, false, sb));
         y_forward_p(c, rep, sb);
@@ -797,7 +819,7 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
     }
     // look-ahead step (gradient.hpp:438-441)
     StepIO rio;
-    rio.enf = SparseEnforce{n_shell, c.shell_pos, shell_row(last - 1), static_cast<float>(c.ndim)};
+    rio.enf = SparseEnforce{n_shell, c.shell_pos, shell_row(last - 1), static_cast<float>(c.ndim), c.shell_blk8};
     rio.p_out = c.ring[1];
     rio.check_step = 0;
     rio.abs_sign = -1.f;  // replay stepper: absorption_sign = -1 (gradient.hpp:429-431)
@@ -1231,6 +1253,8 @@ int ustfwi_gpu_set_sensors(ustfwi_gpu_ctx* c, size_t n_sensors, const size_t* po
         c->data = nullptr;
         c->sens_pos = c->upload(sp);
         c->sens_idx = c->upload(si);
+        c->release(c->sens_blk8);
+        c->sens_blk8 = upload_blk8(*c, sp);
         c->obs_ready = false;
         ensure_data_buffers(*c);
         // adjoint sources sit at the sensors: contribution s reads q[n*ns + s]

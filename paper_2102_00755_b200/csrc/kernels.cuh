@@ -41,6 +41,7 @@ struct SparseInject {
     const float* w;
     const float* sig;
     const float* scale;
+    const int* blk8 = nullptr;  // blk8[b] = first unique position >= b * 8 rows (row blocks of 8)
 };
 
 // Sparse gather of p (sensor gather simulate.hpp:88-90, shell record :91-95):
@@ -50,6 +51,7 @@ struct SparseGather {
     const int* pos;
     const int* idx;
     float* out;
+    const int* blk8 = nullptr;  // per 8-row block offsets into pos (see SparseInject)
 };
 
 // Dirichlet shell (enforce_shell, engine.hpp:304-307; scaling gradient.hpp:417-427):
@@ -59,7 +61,34 @@ struct SparseEnforce {
     const int* pos;
     const float* vals;
     float ndim;
+    const int* blk8 = nullptr;
 };
+
+// [lo, hi) of the sorted position list inside rows [row0, row0 + nrows): O(1) from the
+// per-8-row-block offsets when the block is 8-row aligned, else a binary search
+__device__ __forceinline__ void sparse_range(const int* pos, int n, const int* blk8, long long row0, int nrows,
+                                             int nz, int& lo, int& hi) {
+    if (n == 0) {
+        lo = hi = 0;
+        return;
+    }
+    if (blk8 && (row0 & 7) == 0) {
+        lo = blk8[row0 >> 3];
+        hi = blk8[(row0 + nrows + 7) >> 3];
+        return;
+    }
+    auto lb = [&](long long key) {
+        int a = 0, b = n;
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            if (pos[mid] < key) a = mid + 1;
+            else b = mid;
+        }
+        return a;
+    };
+    lo = lb(row0 * nz);
+    hi = lb((row0 + nrows) * nz);
+}
 
 // In-kernel c0 correlation (GradientAccumulator, gradient.hpp:146-160,177-182):
 // grad += (2/c0^3) * ((p_new - 2 p_mid) + p_old) / dt * q_adj

@@ -755,25 +755,12 @@ __global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zp_kernel(const __grid_
     const int nrows = (int)min((long long)RW, (long long)(g.x0 + g.xn) * g.ny - row0);
     const long long i0 = row0 * NZ;
     const int lo_key = (int)i0;
-    if (threadIdx.x == 0) {
-        const int hi_key = (int)(i0 + (long long)nrows * NZ);
-        auto lb = [](const int* a, int n, int key) {
-            int lo = 0, hi = n;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (a[mid] < key) lo = mid + 1;
-                else hi = mid;
-            }
-            return lo;
-        };
-        sp[0] = A.inj.n_unique ? lb(A.inj.pos, A.inj.n_unique, lo_key) : 0;
-        sp[1] = A.inj.n_unique ? lb(A.inj.pos, A.inj.n_unique, hi_key) : 0;
-        sp[2] = A.enf.n ? lb(A.enf.pos, A.enf.n, lo_key) : 0;
-        sp[3] = A.enf.n ? lb(A.enf.pos, A.enf.n, hi_key) : 0;
-        sp[4] = A.sens.n ? lb(A.sens.pos, A.sens.n, lo_key) : 0;
-        sp[5] = A.sens.n ? lb(A.sens.pos, A.sens.n, hi_key) : 0;
-        sp[6] = A.shell.n ? lb(A.shell.pos, A.shell.n, lo_key) : 0;
-        sp[7] = A.shell.n ? lb(A.shell.pos, A.shell.n, hi_key) : 0;
+    if (threadIdx.x < 4) {  // one sparse set per thread
+        const int k = threadIdx.x;
+        if (k == 0) sparse_range(A.inj.pos, A.inj.n_unique, A.inj.blk8, row0, nrows, NZ, sp[0], sp[1]);
+        if (k == 1) sparse_range(A.enf.pos, A.enf.n, A.enf.blk8, row0, nrows, NZ, sp[2], sp[3]);
+        if (k == 2) sparse_range(A.sens.pos, A.sens.n, A.sens.blk8, row0, nrows, NZ, sp[4], sp[5]);
+        if (k == 3) sparse_range(A.shell.pos, A.shell.n, A.shell.blk8, row0, nrows, NZ, sp[6], sp[7]);
     }
     for (int i = threadIdx.x; i < M; i += NT) twM[i] = g.pzh.tw[i];
     const int r = threadIdx.x / TPR, lane = threadIdx.x % TPR;
@@ -1197,25 +1184,12 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zp2_kernel(const __grid_c
     const int nrows = (int)min((long long)RW, (long long)(g.x0 + g.xn) * g.ny - row0);
     const long long i0 = row0 * NZ;
     const int lo_key = (int)i0;
-    if (threadIdx.x == 0) {
-        const int hi_key = (int)(i0 + (long long)nrows * NZ);
-        auto lb = [](const int* a, int n, int key) {
-            int lo = 0, hi = n;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (a[mid] < key) lo = mid + 1;
-                else hi = mid;
-            }
-            return lo;
-        };
-        sp[0] = A.inj.n_unique ? lb(A.inj.pos, A.inj.n_unique, lo_key) : 0;
-        sp[1] = A.inj.n_unique ? lb(A.inj.pos, A.inj.n_unique, hi_key) : 0;
-        sp[2] = A.enf.n ? lb(A.enf.pos, A.enf.n, lo_key) : 0;
-        sp[3] = A.enf.n ? lb(A.enf.pos, A.enf.n, hi_key) : 0;
-        sp[4] = A.sens.n ? lb(A.sens.pos, A.sens.n, lo_key) : 0;
-        sp[5] = A.sens.n ? lb(A.sens.pos, A.sens.n, hi_key) : 0;
-        sp[6] = A.shell.n ? lb(A.shell.pos, A.shell.n, lo_key) : 0;
-        sp[7] = A.shell.n ? lb(A.shell.pos, A.shell.n, hi_key) : 0;
+    if (threadIdx.x < 4) {  // one sparse set per thread
+        const int k = threadIdx.x;
+        if (k == 0) sparse_range(A.inj.pos, A.inj.n_unique, A.inj.blk8, row0, nrows, NZ, sp[0], sp[1]);
+        if (k == 1) sparse_range(A.enf.pos, A.enf.n, A.enf.blk8, row0, nrows, NZ, sp[2], sp[3]);
+        if (k == 2) sparse_range(A.sens.pos, A.sens.n, A.sens.blk8, row0, nrows, NZ, sp[4], sp[5]);
+        if (k == 3) sparse_range(A.shell.pos, A.shell.n, A.shell.blk8, row0, nrows, NZ, sp[6], sp[7]);
     }
     for (int i = threadIdx.x; i < M; i += NT) twM[i] = g.pzh.tw[i];
     const int r = threadIdx.x / TPR, t = threadIdx.x % TPR;
