@@ -1438,7 +1438,7 @@ cudaError_t launch_pencil_fast(int axis, bool inv, const GridDev& g, const Penci
                 if (xv == 1) return pencil_sized<480, 32, 8, 2, true>(axis, inv, g, j, st);
                 return pencil_sized<480, 30, 8, 2, true>(axis, inv, g, j, st);
             }
-            return pencil_sized<480, 30, 8, 2, true>(axis, inv, g, j, st);
+            return pencil_sized<480, 30, 8, 2, true>(axis, inv, g, j, st);  // TB 4 / 16: 0.298 / 0.232 ms
         default: return cudaErrorInvalidValue;
     }
 }
