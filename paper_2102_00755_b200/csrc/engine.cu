@@ -1181,13 +1181,18 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
         set_absorption(*c, absorbing ? alpha0 : nullptr, y, c0);
         if (alpha0) c->alpha0_host.assign(alpha0, alpha0 + N);
         else c->alpha0_host.clear();
-        c->gamma_host.clear();
-        if (gamma) {
-            c->gamma_host.assign(gamma, gamma + N);
-            CK(cudaMemcpyAsync(c->gamma, c->gamma_host.data(), N, cudaMemcpyHostToDevice, c->stream));
+        // the boundary shell (shell_indices, medium.hpp:168-178) depends on gamma only: keep
+        // it when the new mask equals the bound one
+        const bool same_gamma = gamma && c->gamma_host.size() == N && std::memcmp(c->gamma_host.data(), gamma, N) == 0;
+        if (!same_gamma) {
+            c->gamma_host.clear();
+            if (gamma) {
+                c->gamma_host.assign(gamma, gamma + N);
+                CK(cudaMemcpyAsync(c->gamma, c->gamma_host.data(), N, cudaMemcpyHostToDevice, c->stream));
+            }
+            c->shell_pos = nullptr;
+            c->shell_thickness = 0;
         }
-        c->shell_pos = nullptr;  // shell depends on gamma
-        c->shell_thickness = 0;
         c->has_medium = true;
         CK(cudaStreamSynchronize(c->stream));
     });

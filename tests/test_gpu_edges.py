@@ -111,3 +111,19 @@ def test_heterogeneous_c0_gradient_matches_oracle(small):
                              [np.asarray(s) for s in src.signals], list(sens.positions), obs, 3, shell)
     assert abs(loss - wl) <= 1e-4 * wl
     assert rel(grad, wg) < 1e-3
+
+
+def test_shell_follows_gamma_changes(small):
+    # the engine keeps the boundary shell while gamma is unchanged and rebuilds it otherwise
+    g, f, pulse, eng = small
+    m = make_homogeneous_medium(g)
+    eng.set_sources(SourceSet([f(5, 5, 5)], [pulse]))
+    eng.set_sensors(SensorArray([f(25, 25, 25)]))
+    sizes = []
+    for r in (6.0, 6.0, 8.0):
+        m.gamma = capi.ball_mask(g.shape, [16, 16, 16], r)
+        eng.set_medium(m)
+        _, trace = eng.forward(2)
+        sizes.append(trace.shape[1])
+        assert trace.shape[1] == len(capi.shell_indices(m.gamma, 2))
+    assert sizes[0] == sizes[1] < sizes[2]
