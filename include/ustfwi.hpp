@@ -4,3 +4,4 @@
 #include "ustfwi/core.hpp"
 #include "ustfwi/solver.hpp"
 #include "ustfwi/gradient.hpp"
+#include "ustfwi/grid.hpp"

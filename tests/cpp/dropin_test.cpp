@@ -1,6 +1,7 @@
 // Drop-in check: reference-style code (test_solver.cpp / gradient.hpp call shapes)
 // compiled against include/ustfwi.hpp and run on the device engine.
 // Build: g++ -std=c++20 -I include tests/cpp/dropin_test.cpp -L paper_2102_00755_b200 -lustfwi_b200
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
@@ -84,6 +85,41 @@ int main() {
     auto real = draw_realization(3, 0.0, g.dt, 20210201, 0, 7);
     auto real2 = draw_realization(3, 0.0, g.dt, 20210201, 0, 7);
     EXPECT(real.weights == real2.weights);
+    // alpha0 gradient (GradientParam::alpha0) through the same call shape
+    {
+        SensorData zero = obs;
+        auto ga = gradient_time_reversal(m, s1, sensors, zero, g, 4, GradientParam::alpha0, &eng);
+        EXPECT(ga.loss > 0.0 && max_abs(ga.grad) > 0.0);
+        bool rho_threw = false;
+        try {
+            gradient_time_reversal(m, s1, sensors, zero, g, 4, GradientParam::rho0, &eng);
+        } catch (const std::invalid_argument&) {
+            rho_threw = true;
+        }
+        EXPECT(rho_threw);
+    }
+    // multigrid transfer (grid/spectral.hpp, grid/filter.hpp): up-down round trip, DC gain
+    {
+        Field f({8, 6, 10});
+        for (std::size_t i = 0; i < f.size(); ++i) f[i] = std::sin(0.37 * static_cast<double>(i));
+        Field up = fourier_interpolate(f, {16, 12, 20});
+        Field back = fourier_interpolate(up, {8, 6, 10});
+        double e = 0, n = 0;
+        for (std::size_t i = 0; i < f.size(); ++i) {
+            e += (back[i] - f[i]) * (back[i] - f[i]);
+            n += f[i] * f[i];
+        }
+        EXPECT(std::sqrt(e / n) < 1e-5);
+        std::vector<double> c(600, 0.5);
+        auto lp = lowpass_filter_timeseries(c, 1e-7, 1e6);
+        EXPECT(std::abs(lp[300] - 0.5) < 1e-5);
+    }
+    // SLBFGS curvature history: one secant pair of a 1-D quadratic gives H g = g / a
+    {
+        LbfgsState H(1);
+        EXPECT(H.push({-1.5}, {-1.5 * 3.7}));
+        EXPECT(std::abs(H.apply({1.3})[0] - 1.3 / 3.7) < 1e-15);
+    }
     std::printf("dropin_test: all checks passed (nt=%d, loss=%.6e)\n", g.nt, gr.loss);
     return 0;
 }
