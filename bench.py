@@ -331,6 +331,19 @@ def b200_arm(a):
     n = g.points
     b_model = n * (BYTES_PER_VU_MODEL * (3 * g.nt - 3) + BYTES_CORR_MODEL * (g.nt - 2))
     path_gbps = b_model / s_per_step / 1e9
+    # the engine's own algorithmic bytes per voxel-update (sum over launch classes) and the
+    # ncu-measured DRAM bytes of the same launches where a launch list is committed
+    alg_bytes = sum(v[2] for v in stats.values())
+    meas_bytes, meas_src = 0.0, None
+    for k, v in stats.items():
+        t, src = ncu_traffic(sc.name, k)
+        if t is None:  # classes without a launch-list entry (small auxiliary kernels): model bytes
+            meas_bytes += v[2]
+            continue
+        meas_bytes += t * v[1]
+        meas_src = src
+    if meas_src is None:
+        meas_bytes = None
     line = {
         "metric": METRIC, "value": value, "unit": "voxel-updates/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
@@ -345,7 +358,12 @@ def b200_arm(a):
                      "algorithmic_bytes_per_launch": d_b / d_n if d_n else 0.0},
         "path_roofline": {"model_bytes_per_gradient": b_model, "model_B_per_voxel_update": b_model / vu,
                           "achieved_GBps": path_gbps, "frac_of_measured": path_gbps / hbm,
-                          "frac_of_8TBps": path_gbps / 8000.0},
+                          "frac_of_8TBps": path_gbps / 8000.0,
+                          "engine_algorithmic_B_per_voxel_update": alg_bytes / vu,
+                          "ncu_dram_B_per_voxel_update": (meas_bytes / vu) if meas_bytes else None,
+                          "ncu_dram_note": (f"{meas_src}: per-class DRAM bytes per launch of the first launches "
+                                            "(forward steps; the replay's correlation traffic is counted at the "
+                                            "forward rate) x launches per gradient") if meas_bytes else None},
         "kernels": kernels,
         "kernel_timing": "CUDA events around every launch of one extra gradient after the timed region "
                          "(adjoint and replay serialised on one stream for that gradient)",
