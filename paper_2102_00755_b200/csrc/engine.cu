@@ -6,6 +6,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -1112,17 +1113,44 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
     return guarded(c, [&] {
         const size_t N = static_cast<size_t>(c->g.N);
         if (!c0 || !rho0) fail(USTFWI_ERR_INVALID, "medium fields must match the grid");
-        // Medium::validate (medium.hpp:41-57)
+        // Medium::validate (medium.hpp:41-57); chunked over host threads, the first failing
+        // check in index order decides the message
+        struct Part {
+            double cmax = 0.0;
+            size_t bad_c0 = SIZE_MAX, bad_rho = SIZE_MAX, bad_a0 = SIZE_MAX;
+            bool absorbing = false;
+        };
+        const size_t hw = std::max<size_t>(1, std::thread::hardware_concurrency());
+        std::vector<Part> parts(hw);
+        std::atomic<size_t> slot{0};
+        ustfwi_host::parallel_chunks(N, [&](size_t b, size_t e) {
+            Part p;
+            for (size_t i = b; i < e; ++i) {
+                if ((c0[i] < c0_min || c0[i] > c0_max) && p.bad_c0 == SIZE_MAX) p.bad_c0 = i;
+                if (!(rho0[i] > 0.0) && p.bad_rho == SIZE_MAX) p.bad_rho = i;
+                if (alpha0) {
+                    if (alpha0[i] < 0.0 && p.bad_a0 == SIZE_MAX) p.bad_a0 = i;
+                    if (alpha0[i] != 0.0) p.absorbing = true;
+                }
+                p.cmax = std::max(p.cmax, c0[i]);
+            }
+            parts[slot.fetch_add(1) % hw] = p;
+        });
         bool absorbing = false;
         double cmax = 0.0;
-        for (size_t i = 0; i < N; ++i) {
-            if (c0[i] < c0_min || c0[i] > c0_max) fail(USTFWI_ERR_INVALID, "c0 outside configured bounds");
-            if (!(rho0[i] > 0.0)) fail(USTFWI_ERR_INVALID, "rho0 must be positive");
-            if (alpha0) {
-                if (alpha0[i] < 0.0) fail(USTFWI_ERR_INVALID, "alpha0 must be non-negative");
-                if (alpha0[i] != 0.0) absorbing = true;
-            }
-            cmax = std::max(cmax, c0[i]);
+        size_t bad_c0 = SIZE_MAX, bad_rho = SIZE_MAX, bad_a0 = SIZE_MAX;
+        for (const Part& p : parts) {
+            cmax = std::max(cmax, p.cmax);
+            absorbing = absorbing || p.absorbing;
+            bad_c0 = std::min(bad_c0, p.bad_c0);
+            bad_rho = std::min(bad_rho, p.bad_rho);
+            bad_a0 = std::min(bad_a0, p.bad_a0);
+        }
+        const size_t first = std::min({bad_c0, bad_rho, bad_a0});
+        if (first != SIZE_MAX) {
+            if (first == bad_c0) fail(USTFWI_ERR_INVALID, "c0 outside configured bounds");
+            if (first == bad_rho) fail(USTFWI_ERR_INVALID, "rho0 must be positive");
+            fail(USTFWI_ERR_INVALID, "alpha0 must be non-negative");
         }
         if (y <= 1.0 || y >= 3.0) fail(USTFWI_ERR_INVALID, "power-law exponent must be in (1,3)");
         // WaveStepper constructor checks (engine.hpp:188-197)
@@ -1134,12 +1162,20 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
         if (cmax * c->grid.dt / min_dx > 2.0 / M_PI * (1.0 + 1e-12))
             fail(USTFWI_ERR_NUMERICAL, "CFL violation: dt exceeds 2/pi * dx / c_max");
         const double dt = c->grid.dt;
-        c->c0_host.assign(c0, c0 + N);
+        c->c0_host.resize(N);
         std::vector<float> c2(N);
-        for (size_t i = 0; i < N; ++i) c2[i] = static_cast<float>(c0[i] * c0[i]);
+        std::atomic<bool> uniform_ok{true};
+        ustfwi_host::parallel_chunks(N, [&](size_t b, size_t e) {
+            std::memcpy(c->c0_host.data() + b, c0 + b, (e - b) * sizeof(double));
+            bool u = true;
+            for (size_t i = b; i < e; ++i) {
+                c2[i] = static_cast<float>(c0[i] * c0[i]);
+                u = u && rho0[i] == rho0[0];
+            }
+            if (!u) uniform_ok = false;
+        });
         CK(cudaMemcpyAsync(c->c0sq, c2.data(), N * sizeof(float), cudaMemcpyHostToDevice, c->stream));
-        bool uniform_rho = true;
-        for (size_t i = 1; i < N && uniform_rho; ++i) uniform_rho = rho0[i] == rho0[0];
+        const bool uniform_rho = uniform_ok;
         c->release(c->dtr_fields);
         c->dtr_fields = nullptr;
         if (uniform_rho) {
@@ -1325,7 +1361,9 @@ int ustfwi_gpu_download_gradient(ustfwi_gpu_ctx* c, double scale_div, double* gr
             std::vector<float> h(N);
             CK(cudaMemcpyAsync(h.data(), c->acc, N * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
-            for (size_t i = 0; i < N; ++i) grad_out[i] = static_cast<double>(h[i]) / scale_div;
+            ustfwi_host::parallel_chunks(N, [&](size_t b, size_t e) {
+                for (size_t i = b; i < e; ++i) grad_out[i] = static_cast<double>(h[i]) / scale_div;
+            });
         }
         if (loss_out) {
             double l[2];

@@ -3,6 +3,8 @@
 
 #include <cstdint>
 #include <string>
+#include <algorithm>
+#include <thread>
 #include <vector>
 
 #include "../../include/ustfwi_capi.h"
@@ -35,6 +37,26 @@ std::vector<uint8_t> erode(const std::vector<uint8_t>& mask, const std::vector<i
 std::vector<size_t> shell_indices(const std::vector<uint8_t>& mask, const std::vector<int>& dims,
                                   int thickness);               // medium.hpp:137-178
 std::vector<double> synth_source_pulse(const ustfwi_grid& g, double frac, double c0_min);
+
+// fn(begin, end) over [0, n) in contiguous chunks on up to hardware_concurrency threads
+// (host-side field conversions at the API boundary; ~59M elements at config D)
+template <class Fn>
+void parallel_chunks(size_t n, Fn&& fn) {
+    const size_t hw = std::max<size_t>(1, std::thread::hardware_concurrency());
+    const size_t nt = std::min<size_t>(hw, std::max<size_t>(1, n / (1u << 20)));
+    if (nt <= 1) {
+        fn(size_t{0}, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    th.reserve(nt);
+    const size_t step = (n + nt - 1) / nt;
+    for (size_t t = 0; t < nt; ++t) {
+        const size_t b = t * step, e = std::min(n, b + step);
+        if (b < e) th.emplace_back([&fn, b, e] { fn(b, e); });
+    }
+    for (auto& x : th) x.join();
+}
 
 // counter-based realization stream (SPEC.md stochastic_estimators RNG contract)
 uint64_t stream_word(uint64_t master_seed, uint64_t iteration, uint64_t index, uint64_t counter);

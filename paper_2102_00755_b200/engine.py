@@ -311,8 +311,6 @@ class GradientResult:
 def gradient_time_reversal(medium: Medium, source: SourceSet, sensors: SensorArray, observed: np.ndarray,
                            grid: UstfwiGrid, boundary_thickness: int, param: str = "c0",
                            engine: Optional[GpuEngine] = None) -> GradientResult:
-    if param != "c0":
-        raise ValueError("only GradientParam::c0 is implemented on the device path")
     if medium.gamma is None:
         raise ValueError("gradient computation requires a gamma mask")
     if observed.shape[1] != grid.nt:
@@ -321,7 +319,7 @@ def gradient_time_reversal(medium: Medium, source: SourceSet, sensors: SensorArr
     eng.set_medium(medium)
     eng.set_sources(source)
     eng.set_sensors(sensors)
-    loss, grad = eng.gradient_tr(observed, boundary_thickness)
+    loss, grad = eng.gradient_tr(observed, boundary_thickness, param=param)
     return GradientResult(loss=loss, grad=grad, boundary_thickness=boundary_thickness)
 
 
