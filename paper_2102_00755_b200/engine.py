@@ -320,7 +320,7 @@ def gradient_time_reversal(medium: Medium, source: SourceSet, sensors: SensorArr
     eng.set_sources(source)
     eng.set_sensors(sensors)
     loss, grad = eng.gradient_tr(observed, boundary_thickness, param=param)
-    return GradientResult(loss=loss, grad=grad, boundary_thickness=boundary_thickness)
+    return GradientResult(loss=loss, grad=grad, param=param, boundary_thickness=boundary_thickness)
 
 
 def evaluate_loss(medium: Medium, source: SourceSet, sensors: SensorArray, observed: np.ndarray,
