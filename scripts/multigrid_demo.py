@@ -1,0 +1,121 @@
+"""BASELINE config 5 / SURVEY §8(d) E: encoded gradients/s on each multigrid level
+(2 / 1 / 0.5 mm) and a short coarse-to-fine reconstruction on the device path
+(`--quick`: the reconstruction part only).
+
+For each level: one encoded TR gradient timed after a warm-up (device + host API, the same
+call a user makes). Then SGD with inertia (§4.4 baseline, beta = 0.5) on the 2 mm
+level with the encoded-gradient estimator (realization i for iteration i; observed data =
+forward of the same encoded source on the truth phantom), the result prolonged to the 1 mm
+interior with the Blackman-tapered Fourier interpolation (multigrid.prolong_model) and
+refined there. (SLBFGS in the raw c0 parameterization is badly scaled for such a short
+run — its first secant pair gives H0 = <s,y>/<y,y> ~ 1e15 — so the paper's
+squared-slowness preconditioning would be needed; the optimizer itself is tested in
+tests/test_gpu_slbfgs.py.) Prints one JSON line."""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2102_00755_b200 import multigrid, scenario  # noqa: E402
+from paper_2102_00755_b200.engine import GpuEngine  # noqa: E402
+from paper_2102_00755_b200.optim import sgd_momentum_run  # noqa: E402
+
+
+def interior_slices(sc):
+    g = sc.grid
+    return tuple(slice(g.pml_size[a], g.shape[a] - g.pml_size[a]) for a in range(3))
+
+
+def rel_err(c, truth, gamma):
+    m = gamma.astype(bool)
+    return float(np.linalg.norm(c[m] - truth[m]) / np.linalg.norm(truth[m]))
+
+
+def estimator(eng, sc, base_c0, gam_idx, cache):
+    def est(u, theta, k):
+        enc = sc.encoded(k)
+        if k not in cache:
+            eng.set_medium(sc.truth)
+            eng.set_sources(enc)
+            cache.clear()
+            cache[k] = eng.forward(0)[0]
+        c0 = base_c0.copy()
+        c0.ravel()[gam_idx] = np.clip(u, 1350.0, 1800.0)
+        m = sc.model
+        m.c0 = c0
+        eng.set_medium(m)
+        eng.set_sources(enc)
+        loss, grad = eng.gradient_tr(cache[k], sc.thickness)
+        return loss, grad.ravel()[gam_idx]
+    return est
+
+
+def main():
+    out = {"levels": {}}
+    quick = "--quick" in sys.argv
+    levels = () if quick else (0, 1, 2)
+    for lv in levels:
+        sc = scenario.config_e(lv)
+        with GpuEngine(sc.grid) as eng:
+            enc = sc.encoded(0)
+            eng.set_medium(sc.truth)
+            eng.set_sources(enc)
+            eng.set_sensors(sc.sensors)
+            obs, _ = eng.forward(0)
+            eng.set_medium(sc.model)
+            eng.gradient_tr(obs, sc.thickness)  # warm-up
+            t0 = time.perf_counter()
+            eng.gradient_tr(obs, sc.thickness)
+            dt = time.perf_counter() - t0
+        out["levels"][sc.name] = {"grid": list(sc.grid.shape), "dx_mm": sc.grid.dx[0] * 1e3, "nt": sc.grid.nt,
+                                  "n_emitters": sc.n_src, "s_per_gradient": dt, "gradients_per_s": 1.0 / dt}
+
+    # coarse-to-fine: 2 mm (6 evaluations), prolong, 1 mm (3 evaluations)
+    hist = []
+    sc0 = scenario.config_e(0)
+    gam0 = np.flatnonzero(np.asarray(sc0.model.gamma).ravel())
+    base0 = np.asarray(sc0.model.c0, dtype=np.float64).copy()
+    with GpuEngine(sc0.grid) as eng:
+        eng.set_sensors(sc0.sensors)
+        est = estimator(eng, sc0, base0, gam0, {})
+        F0, G0 = est(base0.ravel()[gam0], 0.0, 1)
+        nu = 4.0 / np.abs(G0).max()  # steps of a few m/s
+        res0 = sgd_momentum_run(est, base0.ravel()[gam0], 6, nu=nu, beta=0.5, bounds=(1350.0, 1800.0))
+    c_coarse = base0.copy()
+    c_coarse.ravel()[gam0] = res0.u
+    hist.append({"level": sc0.name, "evals": res0.n_evl, "energy": res0.energy,
+                 "rel_l2_start": rel_err(base0, np.asarray(sc0.truth.c0), sc0.model.gamma),
+                 "rel_l2_end": rel_err(c_coarse, np.asarray(sc0.truth.c0), sc0.model.gamma)})
+    sc1 = scenario.config_e(1)
+    s0, s1 = interior_slices(sc0), interior_slices(sc1)
+    fine_int = [sc1.grid.shape[a] - 2 * sc1.grid.pml_size[a] for a in range(3)]
+    up = multigrid.prolong_model(c_coarse[s0], fine_int)
+    c1 = np.asarray(sc1.model.c0, dtype=np.float64).copy()
+    gam1_mask = np.asarray(sc1.model.gamma).astype(bool)
+    c1_int = c1[s1]
+    c1_int[gam1_mask[s1]] = np.clip(up[gam1_mask[s1]], 1350.0, 1800.0)
+    c1[s1] = c1_int
+    gam1 = np.flatnonzero(gam1_mask.ravel())
+    with GpuEngine(sc1.grid) as eng:
+        eng.set_sensors(sc1.sensors)
+        est = estimator(eng, sc1, c1, gam1, {})
+        F1, G1 = est(c1.ravel()[gam1], 0.0, 1)
+        res1 = sgd_momentum_run(est, c1.ravel()[gam1], 3, nu=4.0 / np.abs(G1).max(), beta=0.5,
+                                bounds=(1350.0, 1800.0))
+    c_fine = c1.copy()
+    c_fine.ravel()[gam1] = res1.u
+    water = np.asarray(sc1.model.c0, dtype=np.float64)
+    hist.append({"level": sc1.name, "evals": res1.n_evl, "energy": res1.energy,
+                 "rel_l2_water_init": rel_err(water, np.asarray(sc1.truth.c0), sc1.model.gamma),
+                 "rel_l2_prolonged_init": rel_err(c1, np.asarray(sc1.truth.c0), sc1.model.gamma),
+                 "rel_l2_end": rel_err(c_fine, np.asarray(sc1.truth.c0), sc1.model.gamma)})
+    out["multigrid_reconstruction"] = hist
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
