@@ -495,12 +495,11 @@ template <int AXIS, int TB, bool INV>
 static cudaError_t launch_pencil_t(const GridDev& g, const PencilJobs& jobs, cudaStream_t st) {
     const int L = AXIS == 0 ? g.px.L : g.py.L;
     const size_t smem = (size_t)3 * L * TB * sizeof(float2) + (AXIS == 0 ? (size_t)L * TB * sizeof(float) : 0);
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<unsigned long long> configured{0};
+    once_per_device(configured, [&] {
         cudaFuncSetAttribute(pencil_pass_kernel<AXIS, TB, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              227 * 1024);
-        configured = true;
-    }
+    });
     dim3 grid((g.nzh + TB - 1) / TB, AXIS == 0 ? g.ny : g.nx);
     pencil_pass_kernel<AXIS, TB, INV><<<grid, 256, smem, st>>>(g, jobs);
     return cudaGetLastError();
@@ -548,11 +547,10 @@ cudaError_t launch_zvel(const GridDev& g, float2* S[3], const float2* dz_plus, f
                         const Coef r[3], cudaStream_t st) {
     if (!use_generic_kernels() && fast_rows_supported(g.nz)) return launch_zvel_fast(g, S, dz_plus, v, pml, r, st);
     const int R = zrows_per_cta(g.nz);
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<unsigned long long> configured{0};
+    once_per_device(configured, [&] {
         cudaFuncSetAttribute(zvel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        configured = true;
-    }
+    });
     const unsigned blocks = (unsigned)((g.rows + R - 1) / R);
     zvel_kernel<<<blocks, 256, zsmem_bytes(g.nz, R), st>>>(g, S[0], S[1], S[2], dz_plus, v[0], v[1], v[2], pml,
                                                            r[0], r[1], r[2], R);
@@ -563,12 +561,11 @@ cudaError_t launch_zrho(const GridDev& g, ZrhoArgs a, bool update, cudaStream_t 
     if (update && !use_generic_kernels() && fast_rows_supported(g.nz)) return launch_zrho_fast(g, a, st);
     const int R = zrows_per_cta(g.nz);
     a.rows_per_cta = R;
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<unsigned long long> configured{0};
+    once_per_device(configured, [&] {
         cudaFuncSetAttribute(zrho_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(zrho_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        configured = true;
-    }
+    });
     const unsigned blocks = (unsigned)((g.rows + R - 1) / R);
     if (update) zrho_kernel<true><<<blocks, 256, zsmem_bytes(g.nz, R), st>>>(g, a);
     else zrho_kernel<false><<<blocks, 256, zsmem_bytes(g.nz, R), st>>>(g, a);

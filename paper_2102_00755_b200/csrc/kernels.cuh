@@ -1,6 +1,8 @@
 // Device-side data structures shared by the pass kernels and the host orchestration.
 #pragma once
 
+#include <atomic>
+
 #include <cstdint>
 
 #include <cuda_runtime.h>
@@ -198,6 +200,19 @@ struct AbsArgs {
     int* diverged;
 };
 
+
+// cudaFuncSetAttribute is per device: run `set` once per device that launches the kernel
+// (a process may drive several GPUs, one context each)
+template <class F>
+inline void once_per_device(std::atomic<unsigned long long>& mask, F&& set) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(mask.load() & bit)) {
+        set();
+        mask.fetch_or(bit);
+    }
+}
 
 // ---- launchers (kernels.cu) ---------------------------------------------------------
 int pencil_tile_cols(int L);

@@ -1306,12 +1306,9 @@ template <int AXIS, bool INV, int L, int N1, int TB, int MINB, bool DB>
 cudaError_t run_pencil(const GridDev& g, const PencilJobs& j, cudaStream_t st) {
     using C = PencilCfg<L, N1, TB, DB>;
     auto kern = pencil_fast_kernel<AXIS, INV, L, N1, TB, MINB, DB>;
-    static bool configured = false;
+    static std::atomic<unsigned long long> configured{0};
     constexpr size_t smem = AXIS == 0 ? C::SMEM_X : C::SMEM;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    once_per_device(configured, [&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
     const int ntiles = ((g.nzh + TB - 1) / TB) * (AXIS == 0 ? g.ny : g.xn);
     const int grid = (!DB || ntiles < sm_count() * MINB) ? ntiles : sm_count() * MINB;
     kern<<<grid, C::NT, smem, st>>>(g, j);
@@ -1384,11 +1381,10 @@ cudaError_t run_pencil_tma(const GridDev& g, const PencilJobs& j, cudaStream_t s
     auto kern = pencil_tma_kernel<AXIS, INV, L, N1, TB, MINB, DB>;
     constexpr size_t smem = 128 + ((DB ? 2 : 1) * size_t(L) * TB + size_t(N1) * C::KP + L) * sizeof(float2) +
                             (AXIS == 0 ? size_t(L) * TB * sizeof(float) : 0);
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<unsigned long long> configured{0};
+    once_per_device(configured, [&] {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    });
     const int ntiles = ((g.nzh + TB - 1) / TB) * (AXIS == 0 ? g.ny : g.xn);
     const int grid = (!DB || ntiles < sm_count() * MINB) ? ntiles : sm_count() * MINB;
     kern<<<grid, C::NT, smem, st>>>(g, j, maps);
