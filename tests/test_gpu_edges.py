@@ -127,3 +127,31 @@ def test_shell_follows_gamma_changes(small):
         sizes.append(trace.shape[1])
         assert trace.shape[1] == len(capi.shell_indices(m.gamma, 2))
     assert sizes[0] == sizes[1] < sizes[2]
+
+
+def test_two_engines_in_two_threads_match_sequential():
+    # distinct engines may run concurrently (engine.hpp:14-16): no hidden
+    # shared state in the library (map caches are per thread, attributes per device)
+    import threading
+
+    from paper_2102_00755_b200 import scenario
+    sc = scenario.config_a(nt=60)
+    obs = np.zeros((len(sc.sensors.positions), sc.grid.nt))
+
+    def run(idx, out):
+        with GpuEngine(sc.grid) as eng:
+            eng.set_medium(sc.model)
+            eng.set_sources(sc.encoded(idx))
+            eng.set_sensors(sc.sensors)
+            out[idx] = eng.gradient_tr(obs, 8)
+
+    seq, par = {}, {}
+    for k in (0, 1):
+        run(k, seq)
+    th = [threading.Thread(target=run, args=(k, par)) for k in (0, 1)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for k in (0, 1):
+        assert seq[k][0] == par[k][0] and np.array_equal(seq[k][1], par[k][1])
