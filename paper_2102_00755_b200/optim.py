@@ -124,10 +124,15 @@ def line_search(f: Callable[[np.ndarray], Tuple[float, np.ndarray]], u: np.ndarr
 def slbfgs_run(estimator: Estimator, u0: np.ndarray, n_evl: int, nu: float = 1.0, history: int = 64,
                bounds=None, theta: Callable[[int], float] = lambda i: 0.0,
                weight: Callable[[int], float] = lambda i: float(i) ** 3, do_linesearch: bool = False,
-               device: int = 0, reject_tol: float = 1e-10) -> OptResult:
+               device: int = 0, reject_tol: float = 1e-10, h0: float = 1.0) -> OptResult:
     """Algorithm 2: per iteration two estimator calls with the same
     (theta(i), i), pair (nu z, G_z - G_u), second update z <- z - H_k G_z, projection,
-    J_i = min(F_u, F_z), i^3 averaging from the first energy increase."""
+    J_i = min(F_u, F_z), i^3 averaging from the first energy increase.
+
+    H_0 (an Algorithm 2 input): h0 * I while the buffer is empty, then the standard
+    gamma = <s,y>/<y,y> scaling of the newest pair. The step size nu multiplies
+    both updates, so with gradients not in parameter units keep nu = 1 and put the scale of
+    the first step into h0."""
     u = np.array(u0, dtype=np.float64, copy=True)
     shape = u.shape
     u_bar = np.zeros_like(u)
@@ -141,13 +146,17 @@ def slbfgs_run(estimator: Estimator, u0: np.ndarray, n_evl: int, nu: float = 1.0
     evl = 0
     i = 0
     with DeviceLbfgs(u.size, history, device, reject_tol) as H:
+        def apply_h(g):
+            r = H.apply(g).reshape(shape)
+            return h0 * r if H.pairs()[0] == 0 else r
+
         while evl < n_evl:
             i += 1
             th = theta(i)
             F_u, G_u = estimator(u, th, i)
             evl += 1
             G_u = np.asarray(G_u, dtype=np.float64).reshape(shape)
-            z = -H.apply(G_u).reshape(shape)
+            z = -apply_h(G_u)
             step = nu
             if do_linesearch:
                 F_z, G_z, step, m_evl, _ = line_search(lambda v: estimator(v, th, i), u, z, nu, F_u, G_u)
@@ -157,7 +166,7 @@ def slbfgs_run(estimator: Estimator, u0: np.ndarray, n_evl: int, nu: float = 1.0
             evl += m_evl
             G_z = np.asarray(G_z, dtype=np.float64).reshape(shape)
             accepted = H.push(step * z, G_z - G_u)
-            z = z - H.apply(G_z).reshape(shape)
+            z = z - apply_h(G_z)
             u = _project(u + step * z, bounds)
             J = min(F_u, F_z)
             energy.append(J)

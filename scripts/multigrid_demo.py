@@ -3,14 +3,11 @@
 (`--quick`: the reconstruction part only).
 
 For each level: one encoded TR gradient timed after a warm-up (device + host API, the same
-call a user makes). Then SGD with inertia (§4.4 baseline, beta = 0.5) on the 2 mm
-level with the encoded-gradient estimator (realization i for iteration i; observed data =
-forward of the same encoded source on the truth phantom), the result prolonged to the 1 mm
-interior with the Blackman-tapered Fourier interpolation (multigrid.prolong_model) and
-refined there. (SLBFGS in the raw c0 parameterization is badly scaled for such a short
-run — its first secant pair gives H0 = <s,y>/<y,y> ~ 1e15 — so the paper's
-squared-slowness preconditioning would be needed; the optimizer itself is tested in
-tests/test_gpu_slbfgs.py.) Prints one JSON line."""
+call a user makes). Then SLBFGS (Algorithm 2, optim.slbfgs_run: nu = 1, H0 = h0 I for the
+first step, then the secant scaling) on the 2 mm level with the encoded-gradient estimator
+(realization i for iteration i; observed data = forward of the same encoded source on the
+truth phantom), the result prolonged to the 1 mm interior with the Blackman-tapered Fourier
+interpolation (multigrid.prolong_model) and refined there. Prints one JSON line."""
 import json
 import os
 import sys
@@ -22,7 +19,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2102_00755_b200 import multigrid, scenario  # noqa: E402
 from paper_2102_00755_b200.engine import GpuEngine  # noqa: E402
-from paper_2102_00755_b200.optim import sgd_momentum_run  # noqa: E402
+from paper_2102_00755_b200.optim import slbfgs_run  # noqa: E402
 
 
 def interior_slices(sc):
@@ -74,7 +71,7 @@ def main():
         out["levels"][sc.name] = {"grid": list(sc.grid.shape), "dx_mm": sc.grid.dx[0] * 1e3, "nt": sc.grid.nt,
                                   "n_emitters": sc.n_src, "s_per_gradient": dt, "gradients_per_s": 1.0 / dt}
 
-    # coarse-to-fine: 2 mm (6 evaluations), prolong, 1 mm (3 evaluations)
+    # coarse-to-fine: 2 mm (12 evaluations), prolong, 1 mm (4 evaluations)
     hist = []
     sc0 = scenario.config_e(0)
     gam0 = np.flatnonzero(np.asarray(sc0.model.gamma).ravel())
@@ -83,8 +80,8 @@ def main():
         eng.set_sensors(sc0.sensors)
         est = estimator(eng, sc0, base0, gam0, {})
         F0, G0 = est(base0.ravel()[gam0], 0.0, 1)
-        nu = 4.0 / np.abs(G0).max()  # steps of a few m/s
-        res0 = sgd_momentum_run(est, base0.ravel()[gam0], 6, nu=nu, beta=0.5, bounds=(1350.0, 1800.0))
+        h0 = 2.0 / np.abs(G0).max()  # first step <= 2 m/s
+        res0 = slbfgs_run(est, base0.ravel()[gam0], 12, nu=1.0, h0=h0, bounds=(1350.0, 1800.0))
     c_coarse = base0.copy()
     c_coarse.ravel()[gam0] = res0.u
     hist.append({"level": sc0.name, "evals": res0.n_evl, "energy": res0.energy,
@@ -104,8 +101,7 @@ def main():
         eng.set_sensors(sc1.sensors)
         est = estimator(eng, sc1, c1, gam1, {})
         F1, G1 = est(c1.ravel()[gam1], 0.0, 1)
-        res1 = sgd_momentum_run(est, c1.ravel()[gam1], 3, nu=4.0 / np.abs(G1).max(), beta=0.5,
-                                bounds=(1350.0, 1800.0))
+        res1 = slbfgs_run(est, c1.ravel()[gam1], 4, nu=1.0, h0=2.0 / np.abs(G1).max(), bounds=(1350.0, 1800.0))
     c_fine = c1.copy()
     c_fine.ravel()[gam1] = res1.u
     water = np.asarray(sc1.model.c0, dtype=np.float64)
