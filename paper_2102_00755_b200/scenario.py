@@ -53,6 +53,62 @@ def flat(shape, x, y, z):
     return (int(x) * shape[1] + int(y)) * shape[2] + int(z)
 
 
+def golden_section_placement(n: int, radius: float, center, shape, pml=(0, 0, 0), exclude=None):
+    """golden_section_placement (§4.1 "distribute 2048 transducer
+    locations over the half-sphere by the golden section method"): golden-spiral points on
+    the hemisphere z >= center_z, snapped to the grid inside the PML, duplicates and points in
+    `exclude` dropped, alternately assigned to emitters / receivers. Returns (emitters,
+    receivers) as flat indices."""
+    if n < 2:
+        raise ValueError("n must be >= 2")
+    golden = np.pi * (3.0 - np.sqrt(5.0))
+    cx, cy, cz0 = center
+    emit, recv, seen = [], [], set()
+    ex = None if exclude is None else np.asarray(exclude).ravel()
+    for i in range(n):
+        cz = (i + 0.5) / n
+        st = np.sqrt(max(0.0, 1.0 - cz * cz))
+        phi = golden * i
+        x = int(round(cx + radius * st * np.cos(phi)))
+        y = int(round(cy + radius * st * np.sin(phi)))
+        z = int(round(cz0 + radius * cz))
+        x = min(max(x, pml[0]), shape[0] - pml[0] - 1)
+        y = min(max(y, pml[1]), shape[1] - pml[1] - 1)
+        z = min(max(z, pml[2]), shape[2] - pml[2] - 1)
+        f = flat(shape, x, y, z)
+        if f in seen or (ex is not None and ex[f]):
+            continue
+        seen.add(f)
+        (emit if i % 2 == 0 else recv).append(f)
+    return emit, recv
+
+
+def add_noise(data: np.ndarray, snr_db: float, seed: int) -> np.ndarray:
+    """add_noise (Appendix F): i.i.d. zero-mean Gaussian noise with
+    sigma = RMS(f) * 10^(-SNR/20), RMS over the whole clean dataset; SNR = inf -> unchanged."""
+    f = np.asarray(data, dtype=np.float64)
+    if np.isinf(snr_db) and snr_db > 0:
+        return f.copy()
+    rms = float(np.sqrt(np.mean(f * f))) if f.size else 0.0
+    sigma = rms * 10.0 ** (-snr_db / 20.0)
+    if sigma == 0.0:
+        return f.copy()
+    return f + np.random.default_rng(seed).normal(0.0, sigma, size=f.shape)
+
+
+def per_source_data(engine, sc: "Scenario", medium=None) -> np.ndarray:
+    """Clean SensorData per emitter (ScanScenario): one device forward per
+    source on `medium` (default: the truth phantom) -> [n_src, n_receivers, nt]."""
+    m = sc.truth if medium is None else medium
+    engine.set_medium(m)
+    engine.set_sensors(sc.sensors)
+    out = np.zeros((sc.n_src, len(sc.sensors.positions), sc.grid.nt))
+    for k, (p, sig) in enumerate(zip(sc.sources.positions, sc.sources.signals)):
+        engine.set_sources(SourceSet([p], [sig]))
+        out[k] = engine.forward(0)[0]
+    return out
+
+
 def config_a(nt: Optional[int] = None) -> Scenario:
     """64^3 water, 1 source, 8 sensors, Gaussian bump, ball gamma r=12."""
     interior, dx = [44, 44, 44], 1e-3
@@ -131,24 +187,7 @@ def breast_scenario(name: str, interior, dx: float, n_src: int, nt: Optional[int
     gamma = _ellipsoid(shape, (cx, cy, zw), (a + 2, a + 2, h + 2), zw - 2).astype(np.uint8)
 
     # golden-spiral hemisphere, alternating emitter / receiver
-    n_el = 2 * n_src
-    golden = np.pi * (3.0 - np.sqrt(5.0))
-    emit, recv, seen = [], [], set()
-    for i in range(n_el):
-        cz = (i + 0.5) / n_el
-        st = np.sqrt(max(0.0, 1.0 - cz * cz))
-        phi = golden * i
-        x = int(round(cx + R * st * np.cos(phi)))
-        y = int(round(cy + R * st * np.sin(phi)))
-        z = int(round(zw + R * cz))
-        x = min(max(x, pml[0]), shape[0] - pml[0] - 1)
-        y = min(max(y, pml[1]), shape[1] - pml[1] - 1)
-        z = min(max(z, pml[2]), shape[2] - pml[2] - 1)
-        f = flat(shape, x, y, z)
-        if f in seen or gamma.ravel()[f]:
-            continue
-        seen.add(f)
-        (emit if i % 2 == 0 else recv).append(f)
+    emit, recv = golden_section_placement(2 * n_src, R, (cx, cy, zw), shape, pml, exclude=gamma)
     model = Medium(c0=np.full(shape, WATER), rho0=np.full(shape, 1000.0), gamma=gamma,
                    c0_min=C0_MIN, c0_max=C0_MAX)
     truth = Medium(c0=c0, rho0=np.full(shape, 1000.0), gamma=gamma, c0_min=C0_MIN, c0_max=C0_MAX)
