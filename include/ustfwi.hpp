@@ -5,3 +5,4 @@
 #include "ustfwi/solver.hpp"
 #include "ustfwi/gradient.hpp"
 #include "ustfwi/grid.hpp"
+#include "ustfwi/io.hpp"
