@@ -37,8 +37,7 @@ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // sinc(sqrt(u)) = sum_n (-u)^n / (2n+1)! is entire in u; with u <= 3 (the CFL bound
 // c*dt/dx <= 2/pi gives h|k| <= sqrt(3)) eleven Horner terms are exact to < 1e-9, so no
 // sin / sqrt / division is evaluated per spectral element.
-__device__ __forceinline__ float kappa_fast(float k2, float half_cdt) {
-    const float u = half_cdt * half_cdt * k2;
+__device__ __forceinline__ float kappa_of_u(float u) {
     float s = -1.f / 51090942171709440000.f;  // -1/21!
     s = fmaf(s, u, 1.f / 121645100408832000.f);
     s = fmaf(s, u, -1.f / 355687428096000.f);
@@ -51,6 +50,7 @@ __device__ __forceinline__ float kappa_fast(float k2, float half_cdt) {
     s = fmaf(s, u, 1.f / 6.f);
     return fmaf(-s, u, 1.f);
 }
+__device__ __forceinline__ float kappa_fast(float k2, float half_cdt) { return kappa_of_u(half_cdt * half_cdt * k2); }
 
 // |k|^e multipliers of the absorbing / alpha0 / y paths, kept out of line so the hot x-pass
 // code (kappa) stays compact
@@ -307,12 +307,19 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
     float2* ys = xbuf + NBUF * L * TB;                            // transposed [N1][KP]
     float2* tw = ys + N1 * KP;                                    // W_L^k
     float* kap_s = reinterpret_cast<float*>(tw + L);              // x pass: kappa of the tile
+    float* hkx2_s = kap_s + L * TB;                               // x pass: (h kx)^2 per row
     const FftPlan& plan = AXIS == 0 ? g.px : g.py;
     const bool producer = threadIdx.x == NT - 1;
     if (threadIdx.x == 0) {
         for (int b = 0; b < NBUF; ++b) mbar_init(&bar[b], 1);
     }
     for (int i = threadIdx.x; i < L; i += NT) tw[i] = plan.tw[i];
+    if constexpr (AXIS == 0) {
+        for (int i = threadIdx.x; i < L; i += NT) {
+            const float hk = g.half_cdt * g.kx[i];
+            hkx2_s[i] = hk * hk;
+        }
+    }
 
     int gstart[5];
     int ng = 0;
@@ -447,12 +454,21 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
                         const int kind = jobs.job[gb].kappa;  // one multiplier kind per launch
                         const bool power = kind >= 2;
                         const float e = jobs.job[gb].kexp;
+                        if (power) {
+                            for (int k2 = 0; k2 < N2; ++k2) {
+                                const int k = C::out_row(kb, k2);
+                                const float kx = g.kx[k];
+                                kap_s[k * TB + c] = kpow_mult_call(kx * kx + ky * ky + kz * kz, e, kind);
+                            }
+                        } else {
+                            // u = (h kx)^2 + (h ky)^2 + (h kz)^2, the x term from the shared table
+                            const float hy = g.half_cdt * ky, hz = g.half_cdt * kz;
+                            const float uyz = hy * hy + hz * hz;
 #pragma unroll
-                        for (int k2 = 0; k2 < N2; ++k2) {
-                            const int k = C::out_row(kb, k2);
-                            const float kx = g.kx[k];
-                            const float q2 = kx * kx + ky * ky + kz * kz;
-                            kap_s[k * TB + c] = power ? kpow_mult_call(q2, e, kind) : kappa_fast(q2, g.half_cdt);
+                            for (int k2 = 0; k2 < N2; ++k2) {
+                                const int k = C::out_row(kb, k2);
+                                kap_s[k * TB + c] = kappa_of_u(hkx2_s[k] + uyz);
+                            }
                         }
                     }
 #pragma unroll
@@ -884,6 +900,10 @@ constexpr int pad_mod16(int x, int r) {
     while (x % 16 != r) ++x;
     return x;
 }
+constexpr int pad_mod8(int x, int r) {
+    while (x % 8 != r) ++x;
+    return x;
+}
 
 template <int M, int N1>
 struct Z2 {
@@ -892,10 +912,39 @@ struct Z2 {
     static constexpr int NA = N2 / TPR;
     static constexpr int NZ = 2 * M;
     static constexpr int ZP = N2 + 1;                     // zt: [k1][n2] per row
-    static constexpr int ZT = pad_mod16(N1 * ZP, TPR % 16);  // complex per zt row (rows of a warp on disjoint banks)
+    // complex per zt row. TPR = 8: the two rows of a half-warp are 2 apart (z2_thread), so
+    // ZT = 4 mod 8 puts them 16 banks apart; otherwise consecutive rows on disjoint banks.
+    static constexpr int ZT = TPR == 8 ? pad_mod8(N1 * ZP, 4) : pad_mod16(N1 * ZP, TPR % 16);
     static constexpr int VP = 2 * pad_mod16(M, 4);        // floats per staged real row
     static_assert(N1 % 2 == 0 && N2 % TPR == 0, "paired-residue split");
 };
+
+// Thread -> (row r, residue thread t). 64-bit shared accesses are served per half-warp; with
+// TPR = 8 a half-warp holds two rows and the staged rows have pitches of 8 banks mod 32
+// (nzp = 132 complex, VP = 264 floats), so the half-warp's rows are r and r + 2 (16 banks
+// apart): warp w owns rows 4w + {0, 2, 1, 3}. Other TPR: consecutive rows.
+template <int TPR>
+__device__ __forceinline__ void z2_thread(int tid, int& r, int& t) {
+    if constexpr (TPR == 8) {
+        const int w = tid >> 5, l = tid & 31;
+        r = 4 * w + 2 * ((l >> 3) & 1) + (l >> 4);
+        t = l & 7;
+    } else {
+        r = tid / TPR;
+        t = tid % TPR;
+    }
+}
+
+// Twiddle tables W_M^(k1*n2) in the two layouts the phases read (conflict-free for
+// consecutive t): twA[k1*N2 + n2] (r2c phase A, t -> n2), twB[n2*N1 + r] (c2r phase B, t -> r).
+template <int M, int N1>
+__device__ __forceinline__ void z2_fill_twiddles(const float2* tw, float2* twA, float2* twB, int tid, int nt) {
+    constexpr int N2 = M / N1;
+    for (int i = tid; i < M; i += nt) {
+        twA[i] = tw[(i / N2) * (i % N2)];
+        twB[i] = tw[(i / N1) * (i % N1)];
+    }
+}
 
 // W_{2M}^k as (W_{2M}^r) * (W_{2M}^{N1*k2}), the second factor compile-time
 template <int M, int N1, int K2>
@@ -905,7 +954,7 @@ __device__ __forceinline__ float2 twr_of(float2 wr) {
 
 // c2r phase B of one row: spectrum Xs (shared, >= M+1 bins) -> zt (shared), thread t.
 template <int M, int N1>
-__device__ __forceinline__ void z2_c2r_b(const float2* Xs, const float2* pre, const float2* twM, float2 wr0,
+__device__ __forceinline__ void z2_c2r_b(const float2* Xs, const float2* pre, const float2* twB, float2 wr0,
                                          float2 wr1, int t, float2* zt) {
     using C = Z2<M, N1>;
     constexpr int N2 = C::N2, ZP = C::ZP;
@@ -945,8 +994,8 @@ __device__ __forceinline__ void z2_c2r_b(const float2* Xs, const float2* pre, co
     RDft<N2, true>::run(zb);
 #pragma unroll
     for (int n2 = 0; n2 < N2; ++n2) {
-        zt[r0 * ZP + n2] = n2 ? cmul(za[n2], conjf2(twM[r0 * n2])) : za[n2];
-        zt[r1 * ZP + n2] = n2 ? cmul(zb[n2], conjf2(twM[r1 * n2])) : zb[n2];
+        zt[r0 * ZP + n2] = n2 ? cmul(za[n2], conjf2(twB[n2 * N1 + r0])) : za[n2];
+        zt[r1 * ZP + n2] = n2 ? cmul(zb[n2], conjf2(twB[n2 * N1 + r1])) : zb[n2];
     }
 }
 
@@ -963,11 +1012,11 @@ __device__ __forceinline__ void z2_c2r_a(const float2* zt, int n2, float scale, 
 
 // r2c phase A: pairs u[n1] of codelet n2 -> forward N1 codelet + twiddle -> zt
 template <int M, int N1>
-__device__ __forceinline__ void z2_r2c_a(float2 (&u)[N1], int n2, const float2* twM, float2* zt) {
+__device__ __forceinline__ void z2_r2c_a(float2 (&u)[N1], int n2, const float2* twA, float2* zt) {
     using C = Z2<M, N1>;
     RDft<N1, false>::run(u);
 #pragma unroll
-    for (int k1 = 0; k1 < N1; ++k1) zt[k1 * C::ZP + n2] = k1 ? cmul(u[k1], twM[n2 * k1]) : u[k1];
+    for (int k1 = 0; k1 < N1; ++k1) zt[k1 * C::ZP + n2] = k1 ? cmul(u[k1], twA[k1 * C::N2 + n2]) : u[k1];
 }
 
 // r2c phase B + split: zt -> half spectrum X[0..M] written to Xs (thread t's bins)
@@ -1005,7 +1054,7 @@ struct Z2Smem {
     using C = Z2<M, N1>;
     static constexpr size_t head = 128;  // mbarrier
     static size_t bytes(int nzp, int nreal) {
-        return head + size_t(M) * 8 + size_t(M + 2) * 8 + size_t(RW) * nzp * 8 + size_t(RW) * C::ZT * 8 +
+        return head + size_t(2 * M) * 8 + size_t(M + 2) * 8 + size_t(RW) * nzp * 8 + size_t(RW) * C::ZT * 8 +
                size_t(nreal) * RW * C::VP * 4;
     }
 };
@@ -1021,8 +1070,9 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zvel2_kernel(const __grid
     const int a = blockIdx.y;
     const bool coef_field = A.r[a].field != nullptr;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm_raw);
-    float2* twM = reinterpret_cast<float2*>(sm_raw + 128);
-    float2* pre = twM + M;                       // D_z+ table (axis 2)
+    float2* twA = reinterpret_cast<float2*>(sm_raw + 128);
+    float2* twB = twA + M;
+    float2* pre = twB + M;                       // D_z+ table (axis 2)
     float2* sS = pre + (M + 2);  // keep 16-B alignment for the bulk copies                  // [RW][nzp]
     float2* zt = sS + RW * g.nzp;                // [RW][ZT]
     float* sV = reinterpret_cast<float*>(zt + RW * C::ZT);  // [RW][VP]
@@ -1045,10 +1095,11 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zvel2_kernel(const __grid
             if (coef_field) bulk_g2s(sR + i * VP, A.r[a].field + (row0 + i) * NZ, NZ * 4u, bar);
         }
     }
-    for (int i = threadIdx.x; i < M; i += NT) twM[i] = g.pzh.tw[i];
+    z2_fill_twiddles<M, N1>(g.pzh.tw, twA, twB, threadIdx.x, NT);
     if (a == 2)
         for (int i = threadIdx.x; i <= M; i += NT) pre[i] = A.dz_plus[i];
-    const int r = threadIdx.x / TPR, t = threadIdx.x % TPR;
+    int r, t;
+    z2_thread<TPR>(threadIdx.x, r, t);
     const bool rowok = r < nrows;
     const long long row = row0 + r;
     const int x = rowok ? (int)(row / g.ny) : 0, y = rowok ? (int)(row % g.ny) : 0;
@@ -1057,7 +1108,7 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zvel2_kernel(const __grid
     __syncthreads();
     mbar_wait(bar, 0);
 
-    if (rowok) z2_c2r_b<M, N1>(sS + r * g.nzp, a == 2 ? pre : nullptr, twM, wr0, wr1, t, ztr);
+    if (rowok) z2_c2r_b<M, N1>(sS + r * g.nzp, a == 2 ? pre : nullptr, twB, wr0, wr1, t, ztr);
     __syncthreads();
     if (rowok) {
         const float pa = a == 0 ? __ldg(A.pml.prof[0] + x) : (a == 1 ? __ldg(A.pml.prof[1] + y) : 0.f);
@@ -1082,7 +1133,7 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zvel2_kernel(const __grid
                 *reinterpret_cast<float2*>(va + row * NZ + 2 * n) = vv;
                 u[n1] = vv;
             }
-            z2_r2c_a<M, N1>(u, n2, twM, ztr);  // the same zt entries this thread just read
+            z2_r2c_a<M, N1>(u, n2, twA, ztr);  // the same zt entries this thread just read
         }
     }
     __syncthreads();
@@ -1101,8 +1152,9 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const _
     const int a = blockIdx.y;
     const bool coef_field = A.dtrho0.field != nullptr;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm_raw);
-    float2* twM = reinterpret_cast<float2*>(sm_raw + 128);
-    float2* pre = twM + M;
+    float2* twA = reinterpret_cast<float2*>(sm_raw + 128);
+    float2* twB = twA + M;
+    float2* pre = twB + M;
     float2* sS = pre + (M + 2);  // keep 16-B alignment for the bulk copies
     float2* zt = sS + RW * g.nzp;
     float* sR = reinterpret_cast<float*>(zt + RW * C::ZT);  // rho_a rows
@@ -1124,10 +1176,11 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const _
             if (coef_field) bulk_g2s(sD + i * VP, A.dtrho0.field + (row0 + i) * NZ, NZ * 4u, bar);
         }
     }
-    for (int i = threadIdx.x; i < M; i += NT) twM[i] = g.pzh.tw[i];
+    z2_fill_twiddles<M, N1>(g.pzh.tw, twA, twB, threadIdx.x, NT);
     if (a == 2)
         for (int i = threadIdx.x; i <= M; i += NT) pre[i] = A.dz_minus[i];
-    const int r = threadIdx.x / TPR, t = threadIdx.x % TPR;
+    int r, t;
+    z2_thread<TPR>(threadIdx.x, r, t);
     const bool rowok = r < nrows;
     const long long row = row0 + r;
     const int x = rowok ? (int)(row / g.ny) : 0, y = rowok ? (int)(row % g.ny) : 0;
@@ -1136,7 +1189,7 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const _
     __syncthreads();
     mbar_wait(bar, 0);
 
-    if (rowok) z2_c2r_b<M, N1>(sS + r * g.nzp, a == 2 ? pre : nullptr, twM, wr0, wr1, t, ztr);
+    if (rowok) z2_c2r_b<M, N1>(sS + r * g.nzp, a == 2 ? pre : nullptr, twB, wr0, wr1, t, ztr);
     __syncthreads();
     if (rowok) {
         const float pa = a == 0 ? __ldg(A.pml.prof[0] + x) : (a == 1 ? __ldg(A.pml.prof[1] + y) : 0.f);
@@ -1177,8 +1230,8 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zp2_kernel(const __grid_c
     extern __shared__ __align__(128) unsigned char sm_raw[];
     const GridDev& g = P.g;
     const ZrhoArgs& A = P.a;
-    float2* twM = reinterpret_cast<float2*>(sm_raw);
-    float2* zt = twM + M;
+    float2* twA = reinterpret_cast<float2*>(sm_raw);  // r2c only: one table
+    float2* zt = twA + M;
     __shared__ int sp[8];
     const long long row0 = (long long)g.x0 * g.ny + (long long)blockIdx.x * RW;
     const int nrows = (int)min((long long)RW, (long long)(g.x0 + g.xn) * g.ny - row0);
@@ -1191,8 +1244,9 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zp2_kernel(const __grid_c
         if (k == 2) sparse_range(A.sens.pos, A.sens.n, A.sens.blk8, row0, nrows, NZ, sp[4], sp[5]);
         if (k == 3) sparse_range(A.shell.pos, A.shell.n, A.shell.blk8, row0, nrows, NZ, sp[6], sp[7]);
     }
-    for (int i = threadIdx.x; i < M; i += NT) twM[i] = g.pzh.tw[i];
-    const int r = threadIdx.x / TPR, t = threadIdx.x % TPR;
+    for (int i = threadIdx.x; i < M; i += NT) twA[i] = g.pzh.tw[(i / N2) * (i % N2)];
+    int r, t;
+    z2_thread<TPR>(threadIdx.x, r, t);
     const bool rowok = r < nrows;
     const long long row = row0 + r;
     float2* ztr = zt + r * C::ZT;
@@ -1277,7 +1331,7 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zp2_kernel(const __grid_c
         for (int q = sp[6]; q < sp[7]; ++q) gather(A.shell.pos[q], A.shell.out + q);
         // forward r2c of p into S0
 #pragma unroll
-        for (int j = 0; j < NA; ++j) z2_r2c_a<M, N1>(pv[j], t + TPR * j, twM, ztr);
+        for (int j = 0; j < NA; ++j) z2_r2c_a<M, N1>(pv[j], t + TPR * j, twA, ztr);
     }
     __syncthreads();
     if (rowok) {
@@ -1380,7 +1434,7 @@ cudaError_t run_pencil_tma(const GridDev& g, const PencilJobs& j, cudaStream_t s
         if (j.buf[f] && !pencil_map(&maps.tm[f], j.buf[f], g, AXIS, TB, BOXR)) return cudaErrorInvalidValue;
     auto kern = pencil_tma_kernel<AXIS, INV, L, N1, TB, MINB, DB>;
     constexpr size_t smem = 128 + ((DB ? 2 : 1) * size_t(L) * TB + size_t(N1) * C::KP + L) * sizeof(float2) +
-                            (AXIS == 0 ? size_t(L) * TB * sizeof(float) : 0);
+                            (AXIS == 0 ? size_t(L) * (TB + 1) * sizeof(float) : 0);
     static std::atomic<unsigned long long> configured{0};
     once_per_device(configured, [&] {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
