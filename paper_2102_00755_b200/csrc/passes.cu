@@ -952,24 +952,27 @@ __device__ __forceinline__ float2 twr_of(float2 wr) {
     return twmul<2 * M, N1 * K2, false>(wr);
 }
 
-// c2r phase B of one row: spectrum Xs (shared, >= M+1 bins) -> zt (shared), thread t.
+// c2r phase B of one row: spectrum Xs (shared, >= M+1 bins) -> zt (shared), thread t. Called
+// by every thread of the CTA: zt may alias the staged spectra of other rows, so the stores
+// wait at a barrier until all rows have read theirs.
 template <int M, int N1>
 __device__ __forceinline__ void z2_c2r_b(const float2* Xs, const float2* pre, const float2* twB, float2 wr0,
-                                         float2 wr1, int t, float2* zt) {
+                                         float2 wr1, int t, float2* zt, bool rowok) {
     using C = Z2<M, N1>;
     constexpr int N2 = C::N2, ZP = C::ZP;
     const int r0 = t, r1 = t == 0 ? N1 / 2 : N1 - t;
     float2 A[N2], B[N2];
+    if (!rowok) Xs = pre = nullptr;
 #pragma unroll
     for (int k2 = 0; k2 < N2; ++k2) {
-        A[k2] = Xs[r0 + N1 * k2];
-        B[k2] = Xs[r1 + N1 * k2];
+        A[k2] = Xs ? Xs[r0 + N1 * k2] : make_float2(0.f, 0.f);
+        B[k2] = Xs ? Xs[r1 + N1 * k2] : make_float2(0.f, 0.f);
         if (pre) {
             A[k2] = cmul(A[k2], pre[r0 + N1 * k2]);
             B[k2] = cmul(B[k2], pre[r1 + N1 * k2]);
         }
     }
-    float2 XM = Xs[M];
+    float2 XM = Xs ? Xs[M] : make_float2(0.f, 0.f);
     if (pre) XM = cmul(XM, pre[M]);
     if (t == 0) {  // DC and Nyquist bins: real parts only (fft.hpp:58-63 keeps the real output)
         A[0].y = 0.f;
@@ -992,6 +995,8 @@ __device__ __forceinline__ void z2_c2r_b(const float2* Xs, const float2* pre, co
     });
     RDft<N2, true>::run(za);
     RDft<N2, true>::run(zb);
+    __syncthreads();
+    if (!rowok) return;
 #pragma unroll
     for (int n2 = 0; n2 < N2; ++n2) {
         zt[r0 * ZP + n2] = n2 ? cmul(za[n2], conjf2(twB[n2 * N1 + r0])) : za[n2];
@@ -1054,7 +1059,8 @@ struct Z2Smem {
     using C = Z2<M, N1>;
     static constexpr size_t head = 128;  // mbarrier
     static size_t bytes(int nzp, int nreal) {
-        return head + size_t(2 * M) * 8 + size_t(M + 2) * 8 + size_t(RW) * nzp * 8 + size_t(RW) * C::ZT * 8 +
+        // the staged spectra and zt share one region (z2_c2r_b)
+        return head + size_t(2 * M) * 8 + size_t(M + 2) * 8 + size_t(RW) * cmax(nzp, C::ZT) * 8 +
                size_t(nreal) * RW * C::VP * 4;
     }
 };
@@ -1073,9 +1079,9 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zvel2_kernel(const __grid
     float2* twA = reinterpret_cast<float2*>(sm_raw + 128);
     float2* twB = twA + M;
     float2* pre = twB + M;                       // D_z+ table (axis 2)
-    float2* sS = pre + (M + 2);  // keep 16-B alignment for the bulk copies                  // [RW][nzp]
-    float2* zt = sS + RW * g.nzp;                // [RW][ZT]
-    float* sV = reinterpret_cast<float*>(zt + RW * C::ZT);  // [RW][VP]
+    float2* sS = pre + (M + 2);  // [RW][nzp]; keep 16-B alignment for the bulk copies
+    float2* zt = sS;             // [RW][ZT], aliases sS (z2_c2r_b)
+    float* sV = reinterpret_cast<float*>(zt + RW * cmax(g.nzp, C::ZT));  // [RW][VP]
     float* sR = sV + RW * VP;                    // [RW][VP] (coefficient field)
     float2* const Sa = A.S[a];
     float* const va = A.v[a];
@@ -1108,7 +1114,7 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zvel2_kernel(const __grid
     __syncthreads();
     mbar_wait(bar, 0);
 
-    if (rowok) z2_c2r_b<M, N1>(sS + r * g.nzp, a == 2 ? pre : nullptr, twB, wr0, wr1, t, ztr);
+    z2_c2r_b<M, N1>(sS + r * g.nzp, a == 2 ? pre : nullptr, twB, wr0, wr1, t, ztr, rowok);
     __syncthreads();
     if (rowok) {
         const float pa = a == 0 ? __ldg(A.pml.prof[0] + x) : (a == 1 ? __ldg(A.pml.prof[1] + y) : 0.f);
@@ -1156,8 +1162,8 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const _
     float2* twB = twA + M;
     float2* pre = twB + M;
     float2* sS = pre + (M + 2);  // keep 16-B alignment for the bulk copies
-    float2* zt = sS + RW * g.nzp;
-    float* sR = reinterpret_cast<float*>(zt + RW * C::ZT);  // rho_a rows
+    float2* zt = sS;             // aliases sS (z2_c2r_b)
+    float* sR = reinterpret_cast<float*>(zt + RW * cmax(g.nzp, C::ZT));  // rho_a rows
     float* sD = sR + RW * VP;                               // dt*rho0 field rows (optional)
     float* const ra = A.rho[a];
     const long long row0 = (long long)g.x0 * g.ny + (long long)blockIdx.x * RW;
@@ -1189,7 +1195,7 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const _
     __syncthreads();
     mbar_wait(bar, 0);
 
-    if (rowok) z2_c2r_b<M, N1>(sS + r * g.nzp, a == 2 ? pre : nullptr, twB, wr0, wr1, t, ztr);
+    z2_c2r_b<M, N1>(sS + r * g.nzp, a == 2 ? pre : nullptr, twB, wr0, wr1, t, ztr, rowok);
     __syncthreads();
     if (rowok) {
         const float pa = a == 0 ? __ldg(A.pml.prof[0] + x) : (a == 1 ? __ldg(A.pml.prof[1] + y) : 0.f);
