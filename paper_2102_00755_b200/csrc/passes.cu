@@ -1058,6 +1058,9 @@ template <int M, int N1, int RW>
 struct Z2Smem {
     using C = Z2<M, N1>;
     static constexpr size_t head = 128;  // mbarrier
+    static size_t bytes_rho(int nzp, int nreal) {  // zrho2_axis_kernel layout
+        return 16 + size_t(M) * 8 + size_t(RW) * cmax(nzp, C::ZT) * 8 + size_t(nreal) * RW * C::VP * 4;
+    }
     static size_t bytes(int nzp, int nreal) {
         // the staged spectra and zt share one region (z2_c2r_b)
         return head + size_t(2 * M) * 8 + size_t(M + 2) * 8 + size_t(RW) * cmax(nzp, C::ZT) * 8 +
@@ -1157,11 +1160,10 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const _
     const ZrhoArgs& A = P.a;
     const int a = blockIdx.y;
     const bool coef_field = A.dtrho0.field != nullptr;
+    // c2r only: one twiddle table, D_z- read through L1 (Z2SmemRho: 6 CTAs / SM at M = 128)
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm_raw);
-    float2* twA = reinterpret_cast<float2*>(sm_raw + 128);
-    float2* twB = twA + M;
-    float2* pre = twB + M;
-    float2* sS = pre + (M + 2);  // keep 16-B alignment for the bulk copies
+    float2* twB = reinterpret_cast<float2*>(sm_raw + 16);
+    float2* sS = twB + M;        // 16-B aligned for the bulk copies
     float2* zt = sS;             // aliases sS (z2_c2r_b)
     float* sR = reinterpret_cast<float*>(zt + RW * cmax(g.nzp, C::ZT));  // rho_a rows
     float* sD = sR + RW * VP;                               // dt*rho0 field rows (optional)
@@ -1182,9 +1184,8 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const _
             if (coef_field) bulk_g2s(sD + i * VP, A.dtrho0.field + (row0 + i) * NZ, NZ * 4u, bar);
         }
     }
-    z2_fill_twiddles<M, N1>(g.pzh.tw, twA, twB, threadIdx.x, NT);
-    if (a == 2)
-        for (int i = threadIdx.x; i <= M; i += NT) pre[i] = A.dz_minus[i];
+    for (int i = threadIdx.x; i < M; i += NT) twB[i] = g.pzh.tw[(i / N1) * (i % N1)];
+    const float2* pre = a == 2 ? A.dz_minus : nullptr;
     int r, t;
     z2_thread<TPR>(threadIdx.x, r, t);
     const bool rowok = r < nrows;
@@ -1195,7 +1196,7 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const _
     __syncthreads();
     mbar_wait(bar, 0);
 
-    z2_c2r_b<M, N1>(sS + r * g.nzp, a == 2 ? pre : nullptr, twB, wr0, wr1, t, ztr, rowok);
+    z2_c2r_b<M, N1>(sS + r * g.nzp, pre, twB, wr0, wr1, t, ztr, rowok);
     __syncthreads();
     if (rowok) {
         const float pa = a == 0 ? __ldg(A.pml.prof[0] + x) : (a == 1 ? __ldg(A.pml.prof[1] + y) : 0.f);
@@ -1529,7 +1530,7 @@ cudaError_t zvel2_run(const GridDev& g, const ZvelFastArgs& a, cudaStream_t st) 
 }
 template <int M, int N1, int RW>
 cudaError_t zrho2_run(const GridDev& g, const ZrhoFastArgs& a, cudaStream_t st) {
-    const size_t smem = Z2Smem<M, N1, RW>::bytes(g.nzp, a.a.dtrho0.field ? 2 : 1);
+    const size_t smem = Z2Smem<M, N1, RW>::bytes_rho(g.nzp, a.a.dtrho0.field ? 2 : 1);
     auto kern = zrho2_axis_kernel<M, N1, RW>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const dim3 blocks((unsigned)(((long long)g.xn * g.ny + RW - 1) / RW), 3);
