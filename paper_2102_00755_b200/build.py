@@ -11,8 +11,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libustfwi_b200.so")
-SOURCES = ["engine.cu", "kernels.cu", "passes.cu", "lbfgs.cu", "resample.cu", "host_setup.cpp"]
-HEADERS = ["fft_smem.cuh", "fft_reg.cuh", "async_copy.cuh", "kernels.cuh", "host_setup.hpp", os.path.join("..", "..", "include", "ustfwi_capi.h")]
+SOURCES = ["engine.cu", "kernels.cu", "passes.cu", "passes_y.cu", "lbfgs.cu", "resample.cu", "host_setup.cpp"]
+HEADERS = ["passes.cu", "fft_smem.cuh", "fft_reg.cuh", "async_copy.cuh", "kernels.cuh", "host_setup.hpp", os.path.join("..", "..", "include", "ustfwi_capi.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-fvisibility=hidden", "--expt-relaxed-constexpr",
@@ -32,16 +32,18 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objs = []
-    for src in SOURCES:
+    objs, procs = [], []
+    for src in SOURCES:  # translation units compile in parallel
         obj = os.path.join(CSRC, os.path.splitext(src)[0] + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
-        if verbose:
-            sys.stderr.write(r.stderr)
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
         objs.append(obj)
+    for src, p in procs:
+        out, err = p.communicate()
+        if p.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{out}\n{err}")
+        if verbose:
+            sys.stderr.write(err)
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", *objs, "-o", tmp, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)

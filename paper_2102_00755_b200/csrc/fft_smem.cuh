@@ -24,8 +24,26 @@ struct FftPlan {
     const float2* tw;            // tw[k] = exp(-2*pi*i*k/L), k in [0, L)
 };
 
-__host__ __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__host__ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// Complex add / subtract. On the device these are the packed fp32 pair instructions of
+// sm_100 (FADD2, per-lane IEEE round-to-nearest like FADD, bit-identical results): one issue
+// instead of two. Measured on B200 (v79): faster x pass and z rows, slower y pass,
+// so the y-pass translation unit (passes_y.cu) defines USTFWI_FFT_SCALAR_ADD. Packed complex
+// multiplies (FMUL2 + FFMA2) were slower in the z rows and are not used.
+__host__ __device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000 && !defined(USTFWI_FFT_SCALAR_ADD)
+    return __fadd2_rn(a, b);
+#else
+    return make_float2(a.x + b.x, a.y + b.y);
+#endif
+}
+__host__ __device__ __forceinline__ float2 csub(float2 a, float2 b) {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000 && !defined(USTFWI_FFT_SCALAR_ADD)
+    return __fadd2_rn(a, make_float2(-b.x, -b.y));
+#else
+    return make_float2(a.x - b.x, a.y - b.y);
+#endif
+}
+// (fma(ax, bx, -ay*by), fma(ax, by, ay*bx))
 __host__ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }

@@ -54,7 +54,7 @@ __device__ __forceinline__ float kappa_fast(float k2, float half_cdt) { return k
 
 // |k|^e multipliers of the absorbing / alpha0 / y paths, kept out of line so the hot x-pass
 // code (kappa) stays compact
-__device__ __noinline__ float kpow_mult_call(float k2, float e, int kind) { return kpow_mult(k2, e, kind); }
+static __device__ __noinline__ float kpow_mult_call(float k2, float e, int kind) { return kpow_mult(k2, e, kind); }
 
 // ======================================================================================
 // Pencil passes (x and y)
@@ -494,6 +494,7 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
     if (producer) bulk_wait_all();
 }
 
+#ifndef USTFWI_PASSES_Y_ONLY  // z rows: main translation unit only
 // ======================================================================================
 // Row (z) passes: real FFT of length nz = 2M through the M-point complex transform
 // ======================================================================================
@@ -1347,6 +1348,8 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zp2_kernel(const __grid_c
     }
 }
 
+#endif  // USTFWI_PASSES_Y_ONLY
+
 // ======================================================================================
 // dispatch
 // ======================================================================================
@@ -1452,19 +1455,42 @@ cudaError_t run_pencil_tma(const GridDev& g, const PencilJobs& j, cudaStream_t s
     return cudaGetLastError();
 }
 
+// x passes are instantiated in the main translation unit, y passes only in passes_y.cu
+// (compiled with USTFWI_FFT_SCALAR_ADD, fft_smem.cuh)
 template <int L, int N1, int TB, int MINB, bool DB>
 cudaError_t pencil_sized(int axis, bool inv, const GridDev& g, const PencilJobs& j, cudaStream_t st) {
-    if (use_pencil_tma()) {
-        if (axis == 0) return run_pencil_tma<0, false, L, N1, TB, MINB, DB>(g, j, st);
+#ifdef USTFWI_PASSES_Y_ONLY
+    if (axis != 1) return cudaErrorInvalidValue;
+    if (use_pencil_tma())
         return inv ? run_pencil_tma<1, true, L, N1, TB, MINB, DB>(g, j, st)
                    : run_pencil_tma<1, false, L, N1, TB, MINB, DB>(g, j, st);
-    }
-    if (axis == 0) return run_pencil<0, false, L, N1, TB, MINB, DB>(g, j, st);
     return inv ? run_pencil<1, true, L, N1, TB, MINB, DB>(g, j, st)
                : run_pencil<1, false, L, N1, TB, MINB, DB>(g, j, st);
+#else
+    if (axis != 0) return cudaErrorInvalidValue;
+    if (use_pencil_tma()) return run_pencil_tma<0, false, L, N1, TB, MINB, DB>(g, j, st);
+    return run_pencil<0, false, L, N1, TB, MINB, DB>(g, j, st);
+#endif
 }
 
 }  // namespace
+
+#ifdef USTFWI_PASSES_Y_ONLY
+cudaError_t launch_pencil_fast_y(bool inv, const GridDev& g, const PencilJobs& j, cudaStream_t st) {
+    constexpr int axis = 1;
+    switch (g.py.L) {
+        case 32: return pencil_sized<32, 2, 16, 4, false>(axis, inv, g, j, st);
+        case 64: return pencil_sized<64, 4, 16, 4, false>(axis, inv, g, j, st);
+        case 96: return pencil_sized<96, 6, 16, 3, false>(axis, inv, g, j, st);
+        case 128: return pencil_sized<128, 8, 16, 3, false>(axis, inv, g, j, st);
+        case 144: return pencil_sized<144, 16, 16, 3, false>(axis, inv, g, j, st);
+        case 256: return pencil_sized<256, 16, 16, 3, false>(axis, inv, g, j, st);
+        case 480: return pencil_sized<480, 30, 8, 2, true>(axis, inv, g, j, st);  // TB 4 / 16: 0.298 / 0.232 ms
+        default: return cudaErrorInvalidValue;
+    }
+}
+#else
+cudaError_t launch_pencil_fast_y(bool inv, const GridDev& g, const PencilJobs& j, cudaStream_t st);
 
 bool fast_pencil_supported(int L) {
     switch (L) {
@@ -1474,8 +1500,8 @@ bool fast_pencil_supported(int L) {
 }
 
 cudaError_t launch_pencil_fast(int axis, bool inv, const GridDev& g, const PencilJobs& j, cudaStream_t st) {
-    const int L = axis == 0 ? g.px.L : g.py.L;
-    switch (L) {
+    if (axis == 1) return launch_pencil_fast_y(inv, g, j, st);
+    switch (g.px.L) {
         case 32: return pencil_sized<32, 2, 16, 4, false>(axis, inv, g, j, st);
         case 64: return pencil_sized<64, 4, 16, 4, false>(axis, inv, g, j, st);
         case 96: return pencil_sized<96, 6, 16, 3, false>(axis, inv, g, j, st);
@@ -1495,7 +1521,7 @@ cudaError_t launch_pencil_fast(int axis, bool inv, const GridDev& g, const Penci
                 if (xv == 1) return pencil_sized<480, 32, 8, 2, true>(axis, inv, g, j, st);
                 return pencil_sized<480, 30, 8, 2, true>(axis, inv, g, j, st);
             }
-            return pencil_sized<480, 30, 8, 2, true>(axis, inv, g, j, st);  // TB 4 / 16: 0.298 / 0.232 ms
+            return cudaErrorInvalidValue;
         default: return cudaErrorInvalidValue;
     }
 }
@@ -1632,5 +1658,7 @@ cudaError_t launch_zrho_fast(const GridDev& g, const ZrhoArgs& a, cudaStream_t s
         default: return cudaErrorInvalidValue;
     }
 }
+
+#endif  // !USTFWI_PASSES_Y_ONLY
 
 }  // namespace ustfwi_dev
