@@ -18,6 +18,11 @@ Fixtures (small, committed):
                       same gradient with GradientOptions::dispersion_enabled = false, the alpha0
                       and y gradients (GradientParam), the alpha0 gradient of the lossless model,
                       y = 2 (no dispersion term) traces
+  config_a_fd.npz     config A (nt=393): loss, the directional derivative <G, delta> of the
+                      TR gradient with the shell = all of gamma (thickness 12), the central finite
+                      difference of evaluate_loss along delta (eps 0.5 m/s), and the relative l2
+                      distance of the thickness-1/2/4/8 TR gradients to the thickness-12 one
+                      (`--fd-only`; ~25 min single-threaded)
 """
 from __future__ import annotations
 
@@ -157,7 +162,43 @@ def config_a_absorb_fixture(nt=96):
           f"{np.linalg.norm(data15 - lossless) / np.linalg.norm(lossless):.3e}")
 
 
+def fd_direction(shape, gamma):
+    """Smooth bump inside gamma, the same formula as tests/test_gpu_gradcheck.py."""
+    c = [n // 2 for n in shape]
+    ix, iy, iz = np.meshgrid(*[np.arange(n) for n in shape], indexing="ij")
+    r2 = (ix - c[0] - 2) ** 2 + (iy - c[1] + 1) ** 2 + (iz - c[2]) ** 2
+    return np.exp(-r2 / (2 * 3.0 ** 2)) * np.asarray(gamma, dtype=np.float64)
+
+
+def config_a_fd_fixture(eps=0.5):
+    from paper_2102_00755_b200.engine import Medium
+    sc = scenario.config_a()
+    g = sc.grid
+    pos, sig, sens = list(sc.sources.positions), list(sc.sources.signals), list(sc.sensors.positions)
+    delta = fd_direction(g.shape, sc.model.gamma)
+    obs, _ = ref.simulate_forward(g, sc.truth, pos, sig, sens)
+    loss, g_full = ref.gradient_time_reversal(g, sc.model, pos, sig, sens, obs, 12)
+    dJ = float(np.sum(g_full * delta))
+    c0 = np.asarray(sc.model.c0, dtype=np.float64)
+
+    def with_c0(cc):
+        m = sc.model
+        return Medium(c0=cc, rho0=m.rho0, gamma=m.gamma, c0_min=m.c0_min, c0_max=m.c0_max)
+    jp = ref.evaluate_loss(g, with_c0(c0 + eps * delta), pos, sig, sens, obs)
+    jm = ref.evaluate_loss(g, with_c0(c0 - eps * delta), pos, sig, sens, obs)
+    errs = []
+    for t in (1, 2, 4, 8):
+        _, gt = ref.gradient_time_reversal(g, sc.model, pos, sig, sens, obs, t)
+        errs.append(float(np.linalg.norm(gt - g_full) / np.linalg.norm(g_full)))
+    np.savez_compressed(os.path.join(OUT, "config_a_fd.npz"), loss=loss, dJ=dJ, fd=(jp - jm) / (2 * eps), eps=eps,
+                        thickness=np.array([1, 2, 4, 8]), tr_err_vs_12=np.array(errs))
+    print(f"config_a_fd: dJ {dJ:.6e} fd {(jp - jm) / (2 * eps):.6e} tr errors {errs}")
+
+
 if __name__ == "__main__":
+    if "--fd-only" in sys.argv:
+        config_a_fd_fixture()
+        sys.exit(0)
     if "--multigrid-only" in sys.argv:
         multigrid_fixture()
         sys.exit(0)
