@@ -1231,8 +1231,14 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const _
 // :304-307), the gathers (simulate.hpp:88-95), the TR correlation (gradient.hpp:177-182)
 // and the r2c of p. Sparse updates are applied by the owner thread of each position straight
 // to the split densities in HBM, in reference order, before that thread reads them.
+#ifndef USTFWI_ZP_CHUNK
+#define USTFWI_ZP_CHUNK 2
+#endif
+#ifndef USTFWI_ZP_MINB
+#define USTFWI_ZP_MINB 8
+#endif
 template <int M, int N1, int RW>
-__global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zp2_kernel(const __grid_constant__ ZrhoFastArgs P) {
+__global__ void __launch_bounds__(RW * Z2<M, N1>::TPR, USTFWI_ZP_MINB) zp2_kernel(const __grid_constant__ ZrhoFastArgs P) {
     using C = Z2<M, N1>;
     constexpr int N2 = C::N2, TPR = C::TPR, NA = C::NA, NZ = C::NZ, NT = RW * TPR;
     extern __shared__ __align__(128) unsigned char sm_raw[];
@@ -1297,30 +1303,45 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zp2_kernel(const __grid_c
 
     float2 pv[NA][N1];
     if (rowok) {
+        // ZPC elements per batch: every stream load of a batch is issued before its first
+        // store (the stores to p_out / grad may alias the streams as far as the compiler
+        // knows, so without batching each element waits out its own load latency). Pairs at
+        // the 64-register cap (8 CTAs / SM, USTFWI_ZP_MINB) measured best: D200 1.705 ->
+        // 1.695 s / gradient; 4 / 8 per batch or an uncapped 80-96 registers were slower
+        constexpr int ZPC = N1 % USTFWI_ZP_CHUNK == 0 ? USTFWI_ZP_CHUNK : (N1 % 2 == 0 ? 2 : 1);
 #pragma unroll
         for (int j = 0; j < NA; ++j) {
             const int n2 = t + TPR * j;
 #pragma unroll
-            for (int n1 = 0; n1 < N1; ++n1) {
-                const long long i = row * NZ + 2 * (n2 + N2 * n1);
-                const float2 q0 = *reinterpret_cast<const float2*>(A.rho[0] + i);
-                const float2 q1 = *reinterpret_cast<const float2*>(A.rho[1] + i);
-                const float2 q2 = *reinterpret_cast<const float2*>(A.rho[2] + i);
-                const float2 c2 = __ldg(reinterpret_cast<const float2*>(A.c0sq + i));
-                float2 p;
-                p.x = c2.x * ((q0.x + q1.x) + q2.x);
-                p.y = c2.y * ((q0.y + q1.y) + q2.y);
-                *reinterpret_cast<float2*>(A.p_out + i) = p;
-                pv[j][n1] = p;
-                if (A.corr.grad != nullptr) {
-                    const float2 pm = *reinterpret_cast<const float2*>(A.corr.p_mid + i);
-                    const float2 po = *reinterpret_cast<const float2*>(A.corr.p_old + i);
-                    const float2 qa = *reinterpret_cast<const float2*>(A.corr.q_adj + i);
-                    float2 gv = *reinterpret_cast<const float2*>(A.corr.grad + i);
-                    const float wx = 2.f / (c2.x * sqrtf(c2.x)), wy = 2.f / (c2.y * sqrtf(c2.y));
-                    gv.x += wx * (((p.x - 2.f * pm.x) + po.x) * A.corr.inv_dt) * qa.x;
-                    gv.y += wy * (((p.y - 2.f * pm.y) + po.y) * A.corr.inv_dt) * qa.y;
-                    *reinterpret_cast<float2*>(A.corr.grad + i) = gv;
+            for (int c0 = 0; c0 < N1; c0 += ZPC) {
+                float2 q0[ZPC], q1[ZPC], q2[ZPC], c2[ZPC];
+#pragma unroll
+                for (int k = 0; k < ZPC; ++k) {
+                    const long long i = row * NZ + 2 * (n2 + N2 * (c0 + k));
+                    q0[k] = *reinterpret_cast<const float2*>(A.rho[0] + i);
+                    q1[k] = *reinterpret_cast<const float2*>(A.rho[1] + i);
+                    q2[k] = *reinterpret_cast<const float2*>(A.rho[2] + i);
+                    c2[k] = __ldg(reinterpret_cast<const float2*>(A.c0sq + i));
+                }
+#pragma unroll
+                for (int k = 0; k < ZPC; ++k) {
+                    const int n1 = c0 + k;
+                    const long long i = row * NZ + 2 * (n2 + N2 * n1);
+                    float2 p;
+                    p.x = c2[k].x * ((q0[k].x + q1[k].x) + q2[k].x);
+                    p.y = c2[k].y * ((q0[k].y + q1[k].y) + q2[k].y);
+                    *reinterpret_cast<float2*>(A.p_out + i) = p;
+                    pv[j][n1] = p;
+                    if (A.corr.grad != nullptr) {
+                        const float2 pm = *reinterpret_cast<const float2*>(A.corr.p_mid + i);
+                        const float2 po = *reinterpret_cast<const float2*>(A.corr.p_old + i);
+                        const float2 qa = *reinterpret_cast<const float2*>(A.corr.q_adj + i);
+                        float2 gv = *reinterpret_cast<const float2*>(A.corr.grad + i);
+                        const float wx = 2.f / (c2[k].x * sqrtf(c2[k].x)), wy = 2.f / (c2[k].y * sqrtf(c2[k].y));
+                        gv.x += wx * (((p.x - 2.f * pm.x) + po.x) * A.corr.inv_dt) * qa.x;
+                        gv.y += wy * (((p.y - 2.f * pm.y) + po.y) * A.corr.inv_dt) * qa.y;
+                        *reinterpret_cast<float2*>(A.corr.grad + i) = gv;
+                    }
                 }
             }
         }
