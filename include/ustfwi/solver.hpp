@@ -131,6 +131,14 @@ public:
     }
     const Grid& grid() const { return grid_; }
     ustfwi_gpu_ctx* ctx() const { return ctx_.get(); }
+    /// Follow the caller's simulation length (Grid::nt): an extended grid of a delayed encoding
+    /// (nt + ceil(tau/dt)) reuses the same engine.
+    void use_nt(int nt) {
+        if (nt != grid_.nt) {
+            detail::check(ustfwi_gpu_set_nt(ctx(), nt));
+            grid_.nt = nt;
+        }
+    }
 
     /// engine.hpp:118-121
     void derivative(const Field& f, int axis, Stagger st, Field& out) {
@@ -196,6 +204,7 @@ inline SimResult simulate_forward(const Medium& medium, const SourceSet& sources
         local.emplace(grid);
         engine = &*local;
     }
+    engine->use_nt(grid.nt);
     engine->bind(medium);
     engine->bind(sources);
     engine->bind(sensors);

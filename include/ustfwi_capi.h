@@ -136,6 +136,10 @@ USTFWI_API int ustfwi_gpu_set_sources(ustfwi_gpu_ctx* ctx, size_t n_src, const s
                            const int32_t* delay_steps);
 /* SensorArray (solver/medium.hpp:88-91). */
 USTFWI_API int ustfwi_gpu_set_sensors(ustfwi_gpu_ctx* ctx, size_t n_sensors, const size_t* pos);
+/* Simulation length of the following forward / gradient calls (Grid::nt, grid.hpp:18):
+ * delayed source encoding runs over the extended duration T + tau, nt_ext = nt +
+ * ceil(tau/dt). Observed data must be re-uploaded afterwards. */
+USTFWI_API int ustfwi_gpu_set_nt(ustfwi_gpu_ctx* ctx, int nt);
 
 /* simulate_forward (solver/simulate.hpp:30-105). data_out: [n_sensors * nt] sensor-major
  * (SensorData, medium.hpp:94-114). If boundary_thickness > 0 the shell trace
@@ -192,13 +196,23 @@ USTFWI_API int ustfwi_gpu_set_profiling(ustfwi_gpu_ctx* ctx, int enable);
 USTFWI_API int ustfwi_gpu_kernel_stats(ustfwi_gpu_ctx* ctx, int kind, double* total_ms,
                                        uint64_t* launches, double* bytes);
 
-/* ---- mini-batch mean over GPUs (SPEC.md average_estimates :314-322; PAPER §4.5) ---- */
+/* ---- mini-batch mean over GPUs (SPEC.md average_estimates :314-322, worker-count
+ *      independence :328,337; PAPER §4.5) ---- */
 /* ncclGetUniqueId into 128 bytes. */
 USTFWI_API int ustfwi_nccl_unique_id(char id_out[128]);
 /* Bind an NCCL communicator (one rank per GPU) to the context. */
 USTFWI_API int ustfwi_gpu_comm_init(ustfwi_gpu_ctx* ctx, const char id[128], int nranks, int rank);
-/* In place: accumulator <- (sum over ranks of accumulator) / batch, loss likewise. */
-USTFWI_API int ustfwi_gpu_allreduce_mean(ustfwi_gpu_ctx* ctx, int batch);
+/* Reserve `slots` per-realization gradient slots on this rank (cleared to zero). A mini-batch
+ * of B realizations over W ranks uses slots = ceil(B / W); realization r runs on rank r mod W
+ * in slot r / W (an idle rank keeps empty slots and still joins the mean). */
+USTFWI_API int ustfwi_gpu_batch_reserve(ustfwi_gpu_ctx* ctx, int slots);
+/* One TR gradient from the uploaded observed data into `slot` (masked gradient + loss). */
+USTFWI_API int ustfwi_gpu_run_gradient_slot(ustfwi_gpu_ctx* ctx, int boundary_thickness, int slot);
+/* Deterministic mean: all-gather every rank's slots (NCCL, when a communicator is bound), sum
+ * the B realizations in realization order in fp64 and scale by 1/B into the accumulator (read
+ * with ustfwi_gpu_download_gradient(ctx, 1, ...)); the loss likewise. The result is
+ * bit-identical for every world size. */
+USTFWI_API int ustfwi_gpu_batch_mean(ustfwi_gpu_ctx* ctx, int batch);
 
 /* ---- SLBFGS curvature history on the device (Algorithm 2 / Appendix D; SPEC.md
  * optimizer: two_loop_recursion, LbfgsState with m_h = 64). fp64 vectors of length n; S, Y

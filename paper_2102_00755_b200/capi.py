@@ -29,7 +29,8 @@ EXPORTS = [
     "ustfwi_gpu_gradient_tr", "ustfwi_gpu_evaluate_loss", "ustfwi_gpu_derivative",
     "ustfwi_gpu_upload_observed", "ustfwi_gpu_run_gradient", "ustfwi_gpu_download_gradient",
     "ustfwi_gpu_accumulator", "ustfwi_gpu_synchronize", "ustfwi_gpu_stream", "ustfwi_gpu_launch_count",
-    "ustfwi_gpu_shell_size", "ustfwi_gpu_set_profiling", "ustfwi_gpu_kernel_stats", "ustfwi_nccl_unique_id", "ustfwi_gpu_comm_init", "ustfwi_gpu_allreduce_mean",
+    "ustfwi_gpu_shell_size", "ustfwi_gpu_set_profiling", "ustfwi_gpu_kernel_stats", "ustfwi_nccl_unique_id", "ustfwi_gpu_comm_init",
+    "ustfwi_gpu_batch_reserve", "ustfwi_gpu_run_gradient_slot", "ustfwi_gpu_batch_mean", "ustfwi_gpu_set_nt",
     "ustfwi_lbfgs_create", "ustfwi_lbfgs_destroy", "ustfwi_lbfgs_reset", "ustfwi_lbfgs_push", "ustfwi_lbfgs_apply",
     "ustfwi_lbfgs_pairs", "ustfwi_fourier_interpolate", "ustfwi_lowpass_timeseries", "ustfwi_restrict_traces",
 ]

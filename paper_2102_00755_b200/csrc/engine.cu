@@ -31,7 +31,7 @@ namespace {
                  std::string(#expr) + ": " + cudaGetErrorString(e_));                          \
     } while (0)
 
-enum { ST_NONE = 0, ST_PLUS = 1, ST_MINUS = 2, ST_SHIFT = 3 };
+enum { ST_NONE = 0, ST_PLUS = 1, ST_MINUS = 2, ST_SHIFT = 3, ST_SHIFTM = 4, ST_COUNT = 5 };
 enum { KIND_Y = 0, KIND_X = 1, KIND_ZVEL = 2, KIND_ZRHO = 3, KIND_AUX = 4 };
 
 struct Sim {
@@ -78,7 +78,7 @@ struct NcclApi {
     void* h = nullptr;
     int (*get_unique_id)(void*) = nullptr;
     int (*comm_init_rank)(void**, int, const void*, int) = nullptr;  // ncclUniqueId passed by value (128 B)
-    int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*all_gather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
     int (*comm_destroy)(void*) = nullptr;
     const char* (*error_string)(int) = nullptr;
 };
@@ -92,11 +92,11 @@ NcclApi& nccl() {
         api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (!api.h) fail(USTFWI_ERR_NCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
         api.get_unique_id = reinterpret_cast<int (*)(void*)>(dlsym(api.h, "ncclGetUniqueId"));
-        api.all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
-            dlsym(api.h, "ncclAllReduce"));
+        api.all_gather = reinterpret_cast<int (*)(const void*, void*, size_t, int, void*, cudaStream_t)>(
+            dlsym(api.h, "ncclAllGather"));
         api.comm_destroy = reinterpret_cast<int (*)(void*)>(dlsym(api.h, "ncclCommDestroy"));
         api.error_string = reinterpret_cast<const char* (*)(int)>(dlsym(api.h, "ncclGetErrorString"));
-        if (!api.get_unique_id || !api.all_reduce || !api.comm_destroy)
+        if (!api.get_unique_id || !api.all_gather || !api.comm_destroy)
             fail(USTFWI_ERR_NCCL, "libnccl.so.2 lacks the expected symbols");
     }
     return api;
@@ -117,7 +117,7 @@ struct ustfwi_gpu_ctx {
     GridDev g{};
     std::vector<void*> allocs;
 
-    float2* dmul[3][4] = {};  // per padded axis: none / plus / minus / shift tables
+    float2* dmul[3][ST_COUNT] = {};  // per padded axis: none / plus / minus / shift +1/2 / shift -1/2 tables
     float* pml_reg[3] = {};
     float* pml_stag[3] = {};
 
@@ -143,12 +143,15 @@ struct ustfwi_gpu_ctx {
     float* tau0 = nullptr;
     float* eta = nullptr;
     std::vector<double> alpha0_host;
+    std::vector<double> rho0_host;  // GradientParam::rho0 (GradientAccumulator, gradient.hpp:117-128)
+    Coef rho0c{};
+    float* rho0_field = nullptr;
     // gradient parameter (GradientParam: 0 c0, 2 alpha0, 3 y) and the accumulator's extra
     // terms (gradient.hpp:56-142): weight fields wa1, wa2, wa1l, wa2l and the replay rings
     int grad_param = 0;
     struct AccPlan {
-        bool ddot = true, a1 = false, a2 = false, a1l = false, a2l = false;
-        bool extra() const { return a1 || a2 || a1l || a2l || !ddot; }
+        bool ddot = true, a1 = false, a2 = false, a1l = false, a2l = false, rho0 = false;
+        bool extra() const { return a1 || a2 || a1l || a2l || rho0 || !ddot; }
     } plan;
     float* acc_mem = nullptr;      // 4 weight fields + 12 ring fields
     float* wa[4] = {};
@@ -193,6 +196,14 @@ struct ustfwi_gpu_ctx {
     size_t trace_elems = 0;
 
     void* comm = nullptr;
+    int nranks = 1, rank = 0;
+    // mini-batch slots (ustfwi_gpu_run_gradient_slot / ustfwi_gpu_batch_mean): per-realization
+    // masked gradients and losses of this rank, and the all-gathered copy of every rank's
+    int n_slots = 0;
+    float* slot_grad = nullptr;     // [n_slots][N]
+    double* slot_loss = nullptr;    // [n_slots]
+    float* gather_grad = nullptr;   // [nranks][n_slots][N]
+    double* gather_loss = nullptr;  // [nranks][n_slots]
 
     // per-launch-class CUDA-event timing (ustfwi_gpu_set_profiling / ustfwi_gpu_kernel_stats)
     struct Pending {
@@ -304,6 +315,13 @@ FftPlan make_plan(Ctx& c, int L) {
 }
 
 long long rows_of(const Ctx& c) { return c.g.rows; }
+
+std::vector<float> to_f32(const double* p, size_t n) {
+    std::vector<float> out(n);
+    for (size_t i = 0; i < n; ++i) out[i] = static_cast<float>(p[i]);
+    return out;
+}
+
 
 void reset_sim(Ctx& c, Sim& s, bool with_p) {
     const size_t nb = static_cast<size_t>(c.g.N) * sizeof(float);
@@ -597,6 +615,22 @@ void ensure_data_buffers(Ctx& c) {
     c.loss_part = c.alloc<double>(std::max(c.n_sens, 1));
 }
 
+// Buffers whose length follows nt (sensor data, observed data, adjoint source) and the
+// adjoint-source injection set at the sensors (contribution s reads q[n*ns + s]); called when
+// the sensors or the simulation length change (ustfwi_gpu_set_nt: the encoded duration
+// T + tau of a delayed realization).
+void rebind_time_buffers(Ctx& c) {
+    for (void* q : {(void*)c.data, (void*)c.obs, (void*)c.q, (void*)c.loss_part}) c.release(q);
+    c.data = nullptr;
+    c.obs_ready = false;
+    ensure_data_buffers(c);
+    const size_t ns = c.sens_pos_host.size();
+    std::vector<int> off(ns), len(ns, c.grid.nt), stride(ns, std::max<int>(1, c.n_sens)), delay(ns, 0);
+    std::iota(off.begin(), off.end(), 0);
+    std::vector<float> w(ns, 1.f);
+    build_inject(c, c.adj, c.sens_pos_host, off, len, stride, delay, w);
+}
+
 void prepare_shell(Ctx& c, int thickness) {
     if (c.gamma_host.empty()) fail(USTFWI_ERR_INVALID, "boundary recording requires a gamma mask");
     if (thickness != c.shell_thickness || !c.shell_pos) {
@@ -676,12 +710,32 @@ void prepare_accumulator(Ctx& c) {
         pl.ddot = false;
         pl.a1 = pl.a1l = true;
         pl.a2 = pl.a2l = disp;
+    } else if (c.grad_param == 1) {
+        // rho0 (gradient.hpp:117-128): the correlation of accumulate_rho0 only; no absorption terms
+        pl.ddot = false;
+        pl.rho0 = true;
     } else {
-        fail(USTFWI_ERR_INVALID, "the device engine computes the c0, alpha0 and y gradients");
+        fail(USTFWI_ERR_INVALID, "unknown gradient parameter");
     }
     c.plan = pl;
     if (!pl.extra()) return;
     const size_t N = static_cast<size_t>(c.g.N);
+    if (pl.rho0) {
+        // rho0 as a coefficient (scalar when uniform) and 5 scratch fields in acc_mem
+        if (!c.acc_mem) c.acc_mem = c.alloc<float>(16 * N);
+        bool uniform = true;
+        for (size_t i = 1; i < N && uniform; ++i) uniform = c.rho0_host[i] == c.rho0_host[0];
+        if (uniform) {
+            c.rho0c = Coef{nullptr, static_cast<float>(c.rho0_host[0])};
+        } else {
+            if (!c.rho0_field) c.rho0_field = c.alloc<float>(N);
+            const auto h = to_f32(c.rho0_host.data(), N);
+            CK(cudaMemcpyAsync(c.rho0_field, h.data(), N * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+            CK(cudaStreamSynchronize(c.stream));
+            c.rho0c = Coef{c.rho0_field, 0.f};
+        }
+        return;
+    }
     if (!c.acc_mem) {
         c.acc_mem = c.alloc<float>(16 * N);
         for (int k = 0; k < 4; ++k) c.wa[k] = c.acc_mem + k * N;
@@ -728,6 +782,59 @@ void prepare_accumulator(Ctx& c) {
     CK(cudaStreamSynchronize(c.stream));
 }
 
+// out = F^-1[ T(k_pa) * (kappa(|k|) if kappa) * F[in] ] through the scratch spectrum s.S[1]:
+// SpectralEngine::derivative (T = D_pa^{+-}, kappa on; engine.hpp:118-121) and half_shift
+// (T = e^{+-i k dx/2}, kappa off; engine.hpp:131-137) on the device passes.
+void spectral_apply(Ctx& c, Sim& s, const float* in, int pa, const float2* tab, int kappa, float* out, cudaStream_t st) {
+    c.count(launch_zfwd(c.g, in, s.S[1], st));
+    PencilJobs j{};
+    j.buf[0] = s.S[1];
+    j.n = 1;
+    j.job[0] = {0, 0, nullptr, 0, 0.f};
+    c.count(launch_pencil(1, false, c.g, j, st));
+    j.job[0] = {0, 0, pa == 0 ? tab : nullptr, kappa, 0.f};
+    c.count(launch_pencil(0, false, c.g, j, st));
+    j.job[0] = {0, 0, pa == 1 ? tab : nullptr, 0, 0.f};
+    c.count(launch_pencil(1, true, c.g, j, st));
+    c.count(launch_zinv(c.g, s.S[1], pa == 2 ? tab : nullptr, out, st));
+}
+
+// GradientAccumulator::accumulate_rho0 (gradient.hpp:213-239) for the replay pressure p (the
+// window centre) and the adjoint pressure q: rq = rho0 q; per axis a: dp = D+_a p,
+// drq = D+_a rq, grad += dt q D-_a(dp / rho~_a) + dt half_shift_{-1}(dp drq / rho~_a^2).
+void rho0_correlate(Ctx& c, Sim& s, const float* p, const float* q, cudaStream_t st) {
+    const long long N = c.g.N;
+    const size_t n = static_cast<size_t>(N);
+    float* rq = c.acc_mem;
+    float* dp = c.acc_mem + n;
+    float* drq = c.acc_mem + 2 * n;
+    float* tmp = c.acc_mem + 3 * n;
+    float* out = c.acc_mem + 4 * n;
+    Rho0Args A{};
+    A.rho0 = c.rho0c;
+    A.dt = static_cast<float>(c.grid.dt);
+    A.inv_dt = static_cast<float>(1.0 / c.grid.dt);
+    A.q = q;
+    A.grad = c.grad;
+    A.dp = dp;
+    A.drq = drq;
+    A.out = out;
+    A.tmp = rq;
+    c.count(launch_rho0_elem(N, 0, A, st));
+    A.tmp = tmp;
+    for (int pa = c.off_axis; pa < 3; ++pa) {
+        A.dtr = c.dtr_stag[pa];
+        spectral_apply(c, s, p, pa, c.dmul[pa][ST_PLUS], 1, dp, st);
+        spectral_apply(c, s, rq, pa, c.dmul[pa][ST_PLUS], 1, drq, st);
+        c.count(launch_rho0_elem(N, 1, A, st));
+        spectral_apply(c, s, tmp, pa, c.dmul[pa][ST_MINUS], 1, out, st);
+        c.count(launch_rho0_elem(N, 2, A, st));
+        c.count(launch_rho0_elem(N, 3, A, st));
+        spectral_apply(c, s, tmp, pa, c.dmul[pa][ST_SHIFTM], 0, out, st);
+        c.count(launch_rho0_elem(N, 4, A, st));
+    }
+}
+
 // GradientAccumulator::push (gradient.hpp:147-160): the multiplier fields of the newest
 // replay pressure ring[slot].
 void acc_push(Ctx& c, Sim& s, int slot, cudaStream_t st) {
@@ -741,6 +848,10 @@ void acc_push(Ctx& c, Sim& s, int slot, cudaStream_t st) {
 
 // GradientAccumulator::accumulate (gradient.hpp:166-203) with newer = slot nw, mid, older.
 void acc_correlate(Ctx& c, Correlate cr, int nw, int mid, int old, cudaStream_t st) {
+    if (c.plan.rho0) {
+        rho0_correlate(c, c.sim[1], c.ring[mid], cr.q_adj, st);
+        return;
+    }
     cr.use_ddot = c.plan.ddot ? 1 : 0;
     cr.dt = static_cast<float>(c.grid.dt);
     if (c.plan.a1) {
@@ -765,7 +876,7 @@ void acc_correlate(Ctx& c, Correlate cr, int nw, int mid, int old, cudaStream_t 
 }
 
 // compute_gradient, TR branch (gradient.hpp:359-462), GradientParam c0 / alpha0 / y.
-void gradient_tr(Ctx& c, int thickness, bool accumulate) {
+void gradient_tr(Ctx& c, int thickness, bool accumulate, int slot = -1) {
     require_medium(c);
     if (c.gamma_host.empty()) fail(USTFWI_ERR_INVALID, "gradient computation requires a gamma mask");
     if (!c.obs_ready) fail(USTFWI_ERR_INVALID, "observed data not uploaded");
@@ -857,6 +968,13 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate) {
         CK(cudaEventRecord(c.ev_join, sb));
         CK(cudaStreamWaitEvent(sa, c.ev_join, 0));
     }
+    if (slot >= 0) {
+        // mini-batch slot: the masked gradient and this realization's loss
+        float* dst = c.slot_grad + static_cast<size_t>(slot) * static_cast<size_t>(c.g.N);
+        c.count(launch_finalize_grad(c.grad, c.gamma, c.g.N, dst, 0, c.flags + 1, c.stream));
+        CK(cudaMemcpyAsync(c.slot_loss + slot, c.loss, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+        return;
+    }
     c.count(launch_finalize_grad(c.grad, c.gamma, c.g.N, c.acc, accumulate ? 1 : 0, c.flags + 1, c.stream));
 }
 
@@ -915,12 +1033,6 @@ int guarded(Ctx* c, Fn&& fn) {
         ustfwi_host::set_last_error(e.what());
         return USTFWI_ERR_INVALID;
     }
-}
-
-std::vector<float> to_f32(const double* p, size_t n) {
-    std::vector<float> out(n);
-    for (size_t i = 0; i < n; ++i) out[i] = static_cast<float>(p[i]);
-    return out;
 }
 
 // fourier_shift(rho0, axis, +1/2) (spectral.hpp:94-112) on the device: the multiplier
@@ -1035,7 +1147,7 @@ int ustfwi_gpu_create(int device, const ustfwi_grid* grid, ustfwi_gpu_ctx** out)
             const auto k = ustfwi_host::wavenumbers(n, dx3[a]);
             std::vector<float> kf(k.begin(), k.end());
             kdev[a] = c->upload(kf);
-            std::vector<float2> tab[4];
+            std::vector<float2> tab[ST_COUNT];
             for (auto& t : tab) t.resize(static_cast<size_t>(n));
             for (int m = 0; m < n; ++m) {
                 const double km = k[static_cast<size_t>(m)];
@@ -1048,8 +1160,10 @@ int ustfwi_gpu_create(int device, const ustfwi_grid* grid, ustfwi_gpu_ctx** out)
                 tab[ST_MINUS][m] = make_float2(static_cast<float>(km * std::sin(h)),
                                                nyq ? 0.f : static_cast<float>(km * std::cos(h)));
                 tab[ST_SHIFT][m] = make_float2(static_cast<float>(std::cos(h)), nyq ? 0.f : static_cast<float>(std::sin(h)));
+                // half_shift direction -1: conj(e^{ikdx/2}), real part on the Nyquist bin (engine.hpp:66-73)
+                tab[ST_SHIFTM][m] = make_float2(static_cast<float>(std::cos(h)), nyq ? 0.f : static_cast<float>(-std::sin(h)));
             }
-            for (int s = 0; s < 4; ++s) c->dmul[a][s] = c->upload(tab[s]);
+            for (int s = 0; s < ST_COUNT; ++s) c->dmul[a][s] = c->upload(tab[s]);
             std::vector<double> r, st;
             if (g3.pml_size[a] > 0) {
                 ustfwi_host::pml_profiles(g3, a, 2.0, r, st);
@@ -1228,6 +1342,7 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
             }
         }
         set_absorption(*c, absorbing ? alpha0 : nullptr, y, c0);
+        c->rho0_host.assign(rho0, rho0 + N);
         if (alpha0) c->alpha0_host.assign(alpha0, alpha0 + N);
         else c->alpha0_host.clear();
         // the boundary shell (shell_indices, medium.hpp:168-178) depends on gamma only: keep
@@ -1239,6 +1354,7 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
                 c->gamma_host.assign(gamma, gamma + N);
                 CK(cudaMemcpyAsync(c->gamma, c->gamma_host.data(), N, cudaMemcpyHostToDevice, c->stream));
             }
+            c->release(c->shell_pos);
             c->shell_pos = nullptr;
             c->shell_thickness = 0;
         }
@@ -1253,9 +1369,7 @@ int ustfwi_gpu_set_gradient_options(ustfwi_gpu_ctx* c, int dispersion_enabled) {
 
 int ustfwi_gpu_set_gradient_param(ustfwi_gpu_ctx* c, int param) {
     return guarded(c, [&] {
-        if (param == 1)
-            fail(USTFWI_ERR_INVALID, "the rho0 gradient is not provided (defective in the reference, SURVEY F3)");
-        if (param != 0 && param != 2 && param != 3) fail(USTFWI_ERR_INVALID, "unknown gradient parameter");
+        if (param < 0 || param > 3) fail(USTFWI_ERR_INVALID, "unknown gradient parameter");
         c->grad_param = param;
     });
 }
@@ -1301,22 +1415,22 @@ int ustfwi_gpu_set_sensors(ustfwi_gpu_ctx* c, size_t n_sensors, const size_t* po
             sp[k] = static_cast<int>(p[static_cast<size_t>(order[k])]);
             si[k] = order[k];
         }
-        for (void* q : {(void*)c->sens_pos, (void*)c->sens_idx, (void*)c->data, (void*)c->obs, (void*)c->q,
-                        (void*)c->loss_part})
-            c->release(q);
-        c->data = nullptr;
+        for (void* q : {(void*)c->sens_pos, (void*)c->sens_idx}) c->release(q);
         c->sens_pos = c->upload(sp);
         c->sens_idx = c->upload(si);
         c->release(c->sens_blk8);
         c->sens_blk8 = upload_blk8(*c, sp);
-        c->obs_ready = false;
-        ensure_data_buffers(*c);
-        // adjoint sources sit at the sensors: contribution s reads q[n*ns + s]
-        std::vector<int> off(n_sensors), len(n_sensors, c->grid.nt), stride(n_sensors, std::max<int>(1, c->n_sens)),
-            delay(n_sensors, 0);
-        std::iota(off.begin(), off.end(), 0);
-        std::vector<float> w(n_sensors, 1.f);
-        build_inject(*c, c->adj, p, off, len, stride, delay, w);
+        rebind_time_buffers(*c);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ustfwi_gpu_set_nt(ustfwi_gpu_ctx* c, int nt) {
+    return guarded(c, [&] {
+        if (nt < 3) fail(USTFWI_ERR_INVALID, "nt must be >= 3");
+        if (nt == c->grid.nt) return;
+        c->grid.nt = nt;
+        rebind_time_buffers(*c);
         CK(cudaStreamSynchronize(c->stream));
     });
 }
@@ -1496,37 +1610,88 @@ int ustfwi_nccl_unique_id(char id_out[128]) {
 
 int ustfwi_gpu_comm_init(ustfwi_gpu_ctx* c, const char id[128], int nranks, int rank) {
     return guarded(c, [&] {
+        if (nranks < 1 || rank < 0 || rank >= nranks) fail(USTFWI_ERR_INVALID, "bad rank / world size");
         auto& api = nccl();
-        if (!api.comm_init_rank) {
-            // ncclCommInitRank(ncclComm_t*, int nranks, ncclUniqueId commId, int rank): the id is
-            // passed by value; declare the exact signature for the call.
-            using Fn = int (*)(void**, int, NcclUniqueId, int);
-            auto fn = reinterpret_cast<Fn>(dlsym(api.h, "ncclCommInitRank"));
-            if (!fn) fail(USTFWI_ERR_NCCL, "ncclCommInitRank missing");
-            NcclUniqueId uid;
-            std::memcpy(uid.internal, id, 128);
-            const int r = fn(&c->comm, nranks, uid, rank);
-            if (r != 0) fail(USTFWI_ERR_NCCL, std::string("ncclCommInitRank: ") + (api.error_string ? api.error_string(r) : "error"));
-            return;
+        // ncclCommInitRank(ncclComm_t*, int nranks, ncclUniqueId commId, int rank): the id is
+        // passed by value (128 bytes)
+        using Fn = int (*)(void**, int, NcclUniqueId, int);
+        auto fn = reinterpret_cast<Fn>(dlsym(api.h, "ncclCommInitRank"));
+        if (!fn) fail(USTFWI_ERR_NCCL, "ncclCommInitRank missing");
+        if (c->comm) {
+            api.comm_destroy(c->comm);
+            c->comm = nullptr;
         }
+        NcclUniqueId uid;
+        std::memcpy(uid.internal, id, 128);
+        const int r = fn(&c->comm, nranks, uid, rank);
+        if (r != 0) {
+            c->comm = nullptr;
+            fail(USTFWI_ERR_NCCL, std::string("ncclCommInitRank: ") + (api.error_string ? api.error_string(r) : "error"));
+        }
+        c->nranks = nranks;
+        c->rank = rank;
     });
 }
 
-int ustfwi_gpu_allreduce_mean(ustfwi_gpu_ctx* c, int batch) {
+int ustfwi_gpu_batch_reserve(ustfwi_gpu_ctx* c, int slots) {
     return guarded(c, [&] {
-        if (!c->comm) fail(USTFWI_ERR_NCCL, "no communicator (ustfwi_gpu_comm_init)");
-        if (batch < 1) fail(USTFWI_ERR_INVALID, "batch must be >= 1");
-        auto& api = nccl();
-        // ncclFloat32 = 7, ncclFloat64 = 8, ncclSum = 0 (nccl.h)
-        int r = api.all_reduce(c->acc, c->acc, static_cast<size_t>(c->g.N), 7, 0, c->comm, c->stream);
-        if (r == 0) r = api.all_reduce(c->loss + 1, c->loss + 1, 1, 8, 0, c->comm, c->stream);
-        if (r != 0) fail(USTFWI_ERR_NCCL, "ncclAllReduce failed");
-        c->count(launch_scale(c->acc, c->g.N, static_cast<float>(1.0 / batch), c->stream));
-        double l = 0.0;
-        CK(cudaMemcpyAsync(&l, c->loss + 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        if (slots < 1) fail(USTFWI_ERR_INVALID, "slots must be >= 1");
+        const size_t N = static_cast<size_t>(c->g.N);
+        if (slots != c->n_slots) {
+            for (void* p : {(void*)c->slot_grad, (void*)c->slot_loss, (void*)c->gather_grad, (void*)c->gather_loss})
+                c->release(p);
+            c->slot_grad = c->alloc<float>(static_cast<size_t>(slots) * N);
+            c->slot_loss = c->alloc<double>(static_cast<size_t>(slots));
+            c->gather_grad = nullptr;
+            c->gather_loss = nullptr;
+            c->n_slots = slots;
+        }
+        // empty slots (idle ranks, ragged batches) hold zeros and are never summed
+        CK(cudaMemsetAsync(c->slot_grad, 0, static_cast<size_t>(slots) * N * sizeof(float), c->stream));
+        CK(cudaMemsetAsync(c->slot_loss, 0, static_cast<size_t>(slots) * sizeof(double), c->stream));
         CK(cudaStreamSynchronize(c->stream));
-        l /= batch;
-        CK(cudaMemcpyAsync(c->loss + 1, &l, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    });
+}
+
+int ustfwi_gpu_run_gradient_slot(ustfwi_gpu_ctx* c, int boundary_thickness, int slot) {
+    return guarded(c, [&] {
+        if (slot < 0 || slot >= c->n_slots) fail(USTFWI_ERR_INVALID, "slot out of range (ustfwi_gpu_batch_reserve)");
+        clear_flags(*c);
+        gradient_tr(*c, boundary_thickness, false, slot);
+        check_flags(*c, true);
+    });
+}
+
+int ustfwi_gpu_batch_mean(ustfwi_gpu_ctx* c, int batch) {
+    return guarded(c, [&] {
+        const int W = c->comm ? c->nranks : 1;
+        const int slots = c->n_slots;
+        if (slots < 1) fail(USTFWI_ERR_INVALID, "no mini-batch slots (ustfwi_gpu_batch_reserve)");
+        if (batch < 1 || batch > W * slots) fail(USTFWI_ERR_INVALID, "batch must be in [1, world * slots]");
+        const size_t N = static_cast<size_t>(c->g.N);
+        const float* gathered = c->slot_grad;
+        const double* gl = c->slot_loss;
+        if (W > 1) {
+            if (!c->gather_grad) {
+                c->gather_grad = c->alloc<float>(static_cast<size_t>(W) * slots * N);
+                c->gather_loss = c->alloc<double>(static_cast<size_t>(W) * slots);
+            }
+            auto& api = nccl();
+            // ncclFloat32 = 7, ncclFloat64 = 8 (nccl.h); rank-major receive layout
+            int r = api.all_gather(c->slot_grad, c->gather_grad, static_cast<size_t>(slots) * N, 7, c->comm, c->stream);
+            if (r == 0) r = api.all_gather(c->slot_loss, c->gather_loss, static_cast<size_t>(slots), 8, c->comm, c->stream);
+            if (r != 0) fail(USTFWI_ERR_NCCL, "ncclAllGather failed");
+            gathered = c->gather_grad;
+            gl = c->gather_loss;
+        }
+        c->count(launch_ordered_mean(c->g.N, gathered, W, slots, batch, c->acc, c->stream));
+        std::vector<double> h(static_cast<size_t>(W) * slots);
+        CK(cudaMemcpyAsync(h.data(), gl, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        double loss = 0.0;
+        for (int q = 0; q < batch; ++q) loss += h[static_cast<size_t>((q % W) * slots + q / W)];
+        loss *= 1.0 / batch;
+        CK(cudaMemcpyAsync(c->loss + 1, &loss, sizeof(double), cudaMemcpyHostToDevice, c->stream));
         CK(cudaStreamSynchronize(c->stream));
     });
 }

@@ -632,6 +632,56 @@ cudaError_t launch_correlate(long long n, const float* p_new, const float* c0sq,
     return cudaGetLastError();
 }
 
+// Elementwise legs of GradientAccumulator::accumulate_rho0 (gradient.hpp:213-239, with the
+// F3 compile fix): mode 0 tmp = rho0 q; 1 tmp = dp / rho~_a; 2 grad += dt out q;
+// 3 tmp = dp drq / rho~_a^2; 4 grad += dt out. 1/rho~_a = (dt/rho~_a) / dt from the
+// stepper's staggered coefficient (WaveStepper constructor, engine.hpp:219-231).
+__global__ void rho0_elem_kernel(long long n, int mode, Rho0Args A) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        switch (mode) {
+            case 0: A.tmp[i] = A.rho0.at(i) * A.q[i]; break;
+            case 1: A.tmp[i] = A.dp[i] * (A.dtr.at(i) * A.inv_dt); break;
+            case 2: A.grad[i] += A.dt * A.out[i] * A.q[i]; break;
+            case 3: {
+                const float ir = A.dtr.at(i) * A.inv_dt;
+                A.tmp[i] = ir * ir * A.dp[i] * A.drq[i];
+                break;
+            }
+            default: A.grad[i] += A.dt * A.out[i]; break;
+        }
+    }
+}
+
+cudaError_t launch_rho0_elem(long long n, int mode, const Rho0Args& a, cudaStream_t st) {
+    rho0_elem_kernel<<<flat_blocks(n), 256, 0, st>>>(n, mode, a);
+    return cudaGetLastError();
+}
+
+// Deterministic mini-batch mean (average_estimates; worker-count independence
+// :328,337): gathered holds W ranks x slots gradients, realization r at rank r mod W, slot
+// r / W; the sum runs in realization order in fp64 and is scaled by 1/B once, so the result
+// is bit-identical for every W.
+__global__ void ordered_mean_kernel(long long n, const float* __restrict__ gathered, int world, int slots,
+                                    int batch, float* __restrict__ out) {
+    const double inv_b = 1.0 / batch;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < batch; ++r) {
+            const long long slot = (long long)(r % world) * slots + r / world;
+            s += (double)gathered[slot * n + i];
+        }
+        out[i] = (float)(s * inv_b);
+    }
+}
+
+cudaError_t launch_ordered_mean(long long n, const float* gathered, int world, int slots, int batch, float* out,
+                                cudaStream_t st) {
+    ordered_mean_kernel<<<flat_blocks(n), 256, 0, st>>>(n, gathered, world, slots, batch, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gather(const float* p, const SparseGather& g, cudaStream_t st) {
     if (g.n <= 0) return cudaSuccess;
     gather_kernel<<<(g.n + 255) / 256, 256, 0, st>>>(p, g);

@@ -201,6 +201,19 @@ struct AbsArgs {
 };
 
 
+// rho0 gradient legs (GradientAccumulator::accumulate_rho0, gradient.hpp:213-239)
+struct Rho0Args {
+    Coef rho0;
+    Coef dtr;             // dt / rho~_a of the axis (staggered density coefficient)
+    float inv_dt, dt;
+    const float* q;       // adjoint pressure
+    const float* dp;
+    const float* drq;
+    const float* out;
+    float* tmp;
+    float* grad;
+};
+
 // cudaFuncSetAttribute is per device: run `set` once per device that launches the kernel
 // (a process may drive several GPUs, one context each)
 template <class F>
@@ -234,6 +247,9 @@ cudaError_t launch_abs_prep(long long n, const AbsArgs& a, cudaStream_t st);
 cudaError_t launch_abs_pressure(long long n, const AbsArgs& a, cudaStream_t st);
 cudaError_t launch_correlate(long long n, const float* p_new, const float* c0sq, const Correlate& c, cudaStream_t st);
 cudaError_t launch_gather(const float* p, const SparseGather& g, cudaStream_t st);
+cudaError_t launch_rho0_elem(long long n, int mode, const Rho0Args& a, cudaStream_t st);
+cudaError_t launch_ordered_mean(long long n, const float* gathered, int world, int slots, int batch, float* out,
+                                cudaStream_t st);
 
 // register-resident fast paths (passes.cu) for the compiled transform lengths
 bool fast_pencil_supported(int L);

@@ -152,6 +152,14 @@ class GpuEngine:
         check(lib().ustfwi_gpu_set_sources(self._h, C.c_size_t(n), ptr(pos, C.c_size_t), ptr(off, C.c_size_t),
                                            ptr(sig, C.c_double), wp, dp))
 
+    def set_nt(self, nt: int):
+        """Simulation length of the following calls (Grid::nt): the encoded duration
+        T + tau of a delayed realization. Observed data must be re-uploaded."""
+        check(lib().ustfwi_gpu_set_nt(self._h, int(nt)))
+        g = capi.UstfwiGrid.from_buffer_copy(self.grid)
+        g.nt = int(nt)
+        self.grid = g
+
     def set_sensors(self, s: SensorArray):
         pos = np.ascontiguousarray(s.positions, dtype=np.uint64)
         check(lib().ustfwi_gpu_set_sensors(self._h, C.c_size_t(len(pos)), ptr(pos, C.c_size_t)))
@@ -260,8 +268,17 @@ class GpuEngine:
         buf = C.create_string_buffer(bytes(unique_id), 128)
         check(lib().ustfwi_gpu_comm_init(self._h, buf, int(nranks), int(rank)))
 
-    def allreduce_mean(self, batch: int):
-        check(lib().ustfwi_gpu_allreduce_mean(self._h, int(batch)))
+    def batch_reserve(self, slots: int):
+        """Per-realization gradient slots of a mini-batch (ustfwi_gpu_batch_reserve)."""
+        check(lib().ustfwi_gpu_batch_reserve(self._h, int(slots)))
+
+    def run_gradient_slot(self, thickness: int, slot: int):
+        check(lib().ustfwi_gpu_run_gradient_slot(self._h, int(thickness), int(slot)))
+
+    def batch_mean(self, batch: int):
+        """Deterministic mean of the batch over every rank's slots into the accumulator
+        (NCCL all-gather + realization-ordered fp64 sum, ustfwi_gpu_batch_mean)."""
+        check(lib().ustfwi_gpu_batch_mean(self._h, int(batch)))
 
 
 def nccl_unique_id() -> bytes:
@@ -336,44 +353,76 @@ def evaluate_loss(medium: Medium, source: SourceSet, sensors: SensorArray, obser
 
 @dataclass
 class EncodingRealization:
-    """w_i in {-1,+1}, d_i in [0,1], tau >= 0, keyed by the RNG stream."""
+    """SPEC.md:277-280: w_i in {-1,+1}, d_i in [0,1], tau >= 0, keyed by the RNG stream;
+    delay_steps = round(d_i tau / dt) (delays quantized to whole time steps)."""
     weights: np.ndarray
     delays_unit: np.ndarray
     delay_steps: np.ndarray
     tau: float
     seed: tuple = field(default_factory=tuple)
+    dt: float = 0.0
+
+    def extension(self) -> int:
+        """ceil(tau / dt): the samples appended to the duration."""
+        return extension_steps(self.tau, self.dt)
+
+
+def extension_steps(tau: float, dt: float) -> int:
+    """ceil(tau/dt), robust to tau being an integer multiple of dt up to rounding."""
+    if tau <= 0.0:
+        return 0
+    if dt <= 0.0:
+        raise ValueError("dt must be positive")
+    return int(np.ceil(tau / dt - 1e-9))
 
 
 def draw_realization(n_src: int, tau: float, dt: float, master_seed: int, iteration: int,
                      index: int) -> EncodingRealization:
     w, d, u = capi.draw_realization(n_src, tau, dt, master_seed, iteration, index)
     return EncodingRealization(weights=w.astype(np.float64), delays_unit=u, delay_steps=d, tau=tau,
-                               seed=(master_seed, iteration, index))
+                               seed=(master_seed, iteration, index), dt=dt)
 
 
 def encode(sources: SourceSet, data: Optional[Sequence[np.ndarray]], r: EncodingRealization, nt: int):
     """s^ = sum w_i s_i(t - d_i tau), f^ = sum w_i f_i(t - d_i tau), both zero
-    padded to nt + ceil(tau/dt) samples (the delay is already quantized in r.delay_steps).
+    padded to nt_ext = nt + ceil(tau/dt) samples (the delay is already quantized in
+    r.delay_steps, each <= ceil(tau/dt)). Errors: tau < 0; a realization of another size; data
+    that is not one [n_sensors, <= nt] array per source on a common sensor array.
     Returns (encoded SourceSet, encoded data [n_sensors, nt_ext] or None, nt_ext)."""
     if r.tau < 0:
         raise ValueError("tau must be non-negative")
-    ext = int(np.max(r.delay_steps)) if len(r.delay_steps) else 0
+    if len(r.weights) != len(sources.positions) or len(r.delay_steps) != len(sources.positions):
+        raise ValueError("realization size does not match the sources")
+    ext = extension_steps(r.tau, r.dt) if r.tau > 0 else 0
+    if len(r.delay_steps) and int(np.max(r.delay_steps)) > ext:
+        raise ValueError("delay exceeds ceil(tau/dt)")
     nt_ext = nt + ext
     enc = SourceSet(positions=list(sources.positions), signals=list(sources.signals),
                     weights=np.asarray(r.weights, np.float64), delays=np.asarray(r.delay_steps, np.int32))
     f_hat = None
     if data is not None:
-        ns = data[0].shape[0]
+        if len(data) != len(sources.positions):
+            raise ValueError("one SensorData per source is required")
+        ns = np.asarray(data[0]).shape[0]
+        for f in data:
+            f = np.asarray(f)
+            if f.ndim != 2 or f.shape[0] != ns or f.shape[1] > nt:
+                raise ValueError("per-source data must be [n_sensors, <= nt] on a common sensor array")
         f_hat = np.zeros((ns, nt_ext))
         for i, f in enumerate(data):
             d = int(r.delay_steps[i])
+            f = np.asarray(f, np.float64)
             f_hat[:, d:d + f.shape[1]] += r.weights[i] * f
     return enc, f_hat, nt_ext
 
 
 def encoded_gradient(engine: GpuEngine, medium: Medium, encoded: SourceSet, sensors: SensorArray,
                      observed: np.ndarray, thickness: int) -> GradientResult:
-    """one TR gradient of the encoded super-source."""
+    """one TR gradient of the encoded super-source over the duration of
+    `observed` (f^, nt_ext = nt + ceil(tau/dt) samples; the engine's nt follows it)."""
+    nt_ext = int(np.asarray(observed).shape[1])
+    if nt_ext != engine.grid.nt:
+        engine.set_nt(nt_ext)
     return gradient_time_reversal(medium, encoded, sensors, observed, engine.grid, thickness, engine=engine)
 
 

@@ -217,4 +217,33 @@ def config_e(level: int, nt=None):
                            nt if nt is not None else nt_paper)
 
 
+def encoding_problem(n_src: int):
+    """Small 3-D source-encoding problem (24^3 interior -> 64^3, up to 4 emitters, 6 receivers,
+    ball gamma r = 8, Gaussian c0 bump): the inputs of the delayed / unbiasedness parity
+    fixtures (tests/golden/make_golden_delayed.py) and tests/test_gpu_encoding.py.
+    Returns (grid, model, truth, emitter positions, receiver positions, pulse)."""
+    interior, dx = [24, 24, 24], 1e-3
+    g = capi.make_grid(interior, dx, C0_MAX, 2 * interior[0] * dx / C0_MIN)
+    shape = g.shape
+    c = [s // 2 for s in shape]
+    gamma = capi.ball_mask(shape, c, 8.0)
+    ix, iy, iz = np.meshgrid(*[np.arange(n) for n in shape], indexing="ij")
+    r2 = (ix - c[0] - 1) ** 2 + (iy - c[1]) ** 2 + (iz - c[2] + 1) ** 2
+    truth_c0 = WATER + 25.0 * np.exp(-r2 / (2 * 3.0 ** 2))
+    model = Medium(c0=np.full(shape, WATER), rho0=np.full(shape, 1000.0), gamma=gamma,
+                   c0_min=C0_MIN, c0_max=C0_MAX)
+    truth = Medium(c0=truth_c0, rho0=np.full(shape, 1000.0), gamma=gamma, c0_min=C0_MIN,
+                   c0_max=C0_MAX)
+    p = g.pml_size[0]
+    src_xyz = [(p + 2, c[1], c[2]), (c[0], p + 2, c[2] + 2), (shape[0] - p - 3, c[1] - 3, c[2]),
+               (c[0] + 2, shape[1] - p - 3, c[2] - 2)][:n_src]
+    srcs = [flat(shape, *q) for q in src_xyz]
+    sens = []
+    for k in range(6):
+        th = np.deg2rad(15.0 + 60.0 * k)
+        sens.append(flat(shape, round(c[0] + 10 * np.cos(th)), round(c[1] + 10 * np.sin(th)), c[2] + 3))
+    pulse = capi.synth_source_pulse(g, 0.8, C0_MIN)
+    return g, model, truth, srcs, sens, pulse
+
+
 CONFIGS = {"A": config_a, "B": config_b, "C": config_c, "D": config_d}
