@@ -103,37 +103,68 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------------
-# CPU reference arm / baseline
+# CPU reference arm / baseline (oracle/_ref only: this path never loads libustfwi_b200.so)
 # ----------------------------------------------------------------------------------------
 
-def _cpu_worker(args):
-    cfg, k = args
+# interior, dx (m), emitters, nt override (the paper's nt at D); the grid itself
+# comes from the reference's own make_grid (grid.hpp:91-103) through oracle/_ref
+CONFIG_SPECS = {"A": ([44, 44, 44], 1e-3, 1, None), "B": ([108, 108, 108], 1e-3, 64, None),
+                "C": ([236, 236, 236], 1e-3, 256, None), "D": ([442, 442, 222], 0.5e-3, 1024, 3912)}
+# resident fp64 bytes per grid point of one ref_time_steps process: engine multipliers and
+# spectra + three steppers + accumulator (measured here: 23.7 GB for a D forward with its
+# shell trace; SURVEY §8(d) estimates 28 GiB for a TR gradient) -> 64 doubles per point
+REF_BYTES_PER_POINT = 64 * 8
+
+
+def ref_grid(cfg: str, nt=None):
     from oracle import ref
-    from paper_2102_00755_b200 import scenario
-    sc = scenario.CONFIGS[cfg](nt=16)
-    t_f, t_p = ref.time_steps(sc.grid, sc.model, k, k)
-    return t_f, t_p, sc.grid.points
+    interior, dx, _, nt_paper = CONFIG_SPECS[cfg]
+    g = ref.make_grid(interior, dx, 1800.0, 2 * max(interior) * dx / 1350.0)
+    if nt is not None:
+        g.nt = int(nt)
+    elif nt_paper:
+        g.nt = int(nt_paper)
+    return g
 
 
-def cpu_reference_sample(cfg: str, k: int, procs: int):
-    """Each process builds the reference SpectralEngine + WaveSteppers (engine.hpp) for the
-    config grid and times k forward steps and k adjoint+replay pair-steps with the
-    GradientAccumulator (oracle/ref_driver.cpp:ref_time_steps). Returns aggregate
-    voxel-updates/s over `procs` concurrent single-threaded processes."""
+def grid_points(g):
+    n = 1
+    for a in range(g.ndim):
+        n *= int(g.dims[a])
+    return n
+
+
+def _cpu_worker(args):
+    cfg, k_fwd, k_pair = args
+    from types import SimpleNamespace
+    from oracle import ref
+    g = ref_grid(cfg, nt=16)
+    shape = tuple(int(g.dims[a]) for a in range(g.ndim))
+    m = SimpleNamespace(c0=np.full(shape, 1500.0), rho0=np.full(shape, 1000.0), alpha0=None, y=1.5, gamma=None,
+                        c0_min=1350.0, c0_max=1800.0)
+    t_f, t_p = ref.time_steps(g, m, k_fwd, k_pair)
+    return t_f, t_p, grid_points(g)
+
+
+def cpu_reference_sample(cfg: str, k_fwd: int, k_pair: int, procs: int):
+    """Each process builds the reference SpectralEngine + WaveSteppers + GradientAccumulator
+    (oracle/ref_driver.cpp:ref_time_steps, engine.hpp / gradient.hpp unmodified) on the config
+    grid and times k_fwd forward steps and k_pair adjoint+replay pair-steps; `procs`
+    single-threaded processes run concurrently (independent realizations). A
+    gradient is nt forward + (nt - 1) replay + (nt - 2) adjoint steps, so one forward step and
+    one pair step advance 3 voxel-update sweeps."""
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     t0 = time.perf_counter()
     with ctx.Pool(procs) as pool:
-        res = pool.map(_cpu_worker, [(cfg, k)] * procs)
+        res = pool.map(_cpu_worker, [(cfg, k_fwd, k_pair)] * procs)
     wall = time.perf_counter() - t0
-    per_proc = [(n * 1 / tf + n * 2 / tp) / 2 for tf, tp, n in res]   # mean of fwd and pair rates
     n = res[0][2]
-    # voxel-updates of one gradient per step: forward nt, pair (nt-2)*2, + 1 look-ahead
     tf = max(r[0] for r in res)
     tp = max(r[1] for r in res)
-    rate_one = n * 3 / (tf + tp)   # one fwd step + one pair step = 3 voxel-update sweeps
+    rate_one = n * 3 / (tf + tp)
     return {"rate_per_core": rate_one, "rate_aggregate": rate_one * procs, "t_fwd_step": tf, "t_pair_step": tp,
-            "points": n, "wall": wall, "per_proc": per_proc}
+            "points": n, "wall": wall}
 
 
 def cpu_cores():
@@ -143,17 +174,73 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def cpu_procs(cfg: str):
-    # footprint per reference process ~ (7 state + 6 scratch + 3 rho~ + 2 medium) fp64 fields +
-    # 15 complex half-spectrum multiplier arrays (engine.hpp:46-78); config B ~ 1 GiB
-    from paper_2102_00755_b200 import scenario
-    n = scenario.CONFIGS[cfg](nt=2).grid.points
-    foot = n * 8 * (18 + 15 + 4)
+def cpu_procs(cfg: str, cap: int = 32):
+    """P = min(nproc, RAM / footprint), capped and with a 0.6 safety factor on
+    the available memory."""
+    n = grid_points(ref_grid(cfg, nt=2))
+    foot = n * REF_BYTES_PER_POINT
     try:
         avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
     except Exception:
         avail = 16 << 30
-    return max(1, min(cpu_cores(), int(0.7 * avail // foot)))
+    return max(1, min(cpu_cores(), cap, int(0.6 * avail // foot)))
+
+
+def fft_impl():
+    """The FFT the oracle links: the in-repo fp64 FFTW-API shim (FFTW3 is not in the image)."""
+    try:
+        out = subprocess.run(["ldconfig", "-p"], capture_output=True, text=True, timeout=10).stdout
+        sys_fftw = "libfftw3.so" in out
+    except Exception:
+        sys_fftw = False
+    return ("in-repo FFTW-API shim (fp64 mixed-radix Stockham, oracle/fftw3_shim)"
+            + ("; a system libfftw3 exists on this host but oracle/_ref was built against the shim" if sys_fftw
+               else "; no libfftw3 on this host"))
+
+
+def cpu_baseline_block(cfg: str, vu_grad: float):
+    """The reference on the benchmarked grid: 1 forward + 1 pair step per process, P processes
+    ('C and D ... extrapolated'), plus the config-B sample beside it."""
+    procs = cpu_procs(cfg)
+    r = cpu_reference_sample(cfg, 1, 1, procs)
+    sample = (f"reference (oracle/_ref: unmodified headers, FFT = {fft_impl()}) on the config {cfg} grid "
+              f"{CONFIG_SPECS[cfg][0]} padded to {r['points']} points: 1 forward + 1 adjoint/replay pair step per "
+              f"process, {procs} concurrent single-threaded processes (P = min(nproc, 0.6 RAM / footprint, 32)); "
+              f"per core {r['rate_per_core']:.3g} vu/s (fwd step {r['t_fwd_step']:.1f} s, pair step "
+              f"{r['t_pair_step']:.1f} s); extrapolated s/gradient {vu_grad / r['rate_aggregate']:.4g}")
+    out = {"value": r["rate_aggregate"], "unit": "voxel-updates/s", "cores": procs, "kind": "reference",
+           "sample": sample, "extrapolated": True, "s_per_gradient_extrapolated": vu_grad / r["rate_aggregate"],
+           "wall_s": r["wall"]}
+    if cfg != "B":
+        pb = cpu_procs("B")
+        rb = cpu_reference_sample("B", 2, 2, pb)
+        out["b_grid_sample"] = {"value": rb["rate_aggregate"], "cores": pb, "per_core": rb["rate_per_core"],
+                                "s_per_gradient_extrapolated": vu_grad / rb["rate_aggregate"],
+                                "sample": "config B grid, 2 fwd + 2 pair steps per process"}
+    return out
+
+
+def ref_config_block(cfg: str, n_gpus: int, batch: int):
+    g = ref_grid(cfg)
+    interior, dx, n_src, _ = CONFIG_SPECS[cfg]
+    n = grid_points(g)
+    return {"workload": f"config {cfg}: source-encoded TR c0 gradient, grid {tuple(int(g.dims[a]) for a in range(3))} "
+                        f"(interior {tuple(interior)}), dx {dx * 1e3:g} mm, nt {g.nt}, {n_src} emitters + "
+                        f"{n_src} receivers, shell thickness 8" + (f", mini-batch of {batch}" if batch else ""),
+            "grid": [int(g.dims[a]) for a in range(3)], "nt": int(g.nt), "n_emitters": n_src,
+            "voxel_updates_per_gradient": n * (3 * int(g.nt) - 3),
+            "parallelism": parallelism(n_gpus, batch), "l2_flush": l2_note(n)}
+
+
+def parallelism(n_gpus, batch):
+    if batch:
+        return f"fixed mini-batch of {batch} encoded realizations over {n_gpus} GPU(s), NCCL all-gather + ordered mean"
+    return f"dp{n_gpus} (one encoded realization per GPU, NCCL all-gather + ordered mean)" if n_gpus > 1 else "1 GPU"
+
+
+def l2_note(points):
+    return ("inputs larger than L2 (each field >= 126 MB)" if points * 4 > 126e6
+            else "working set may be L2-resident at this size")
 
 
 def reference_arm(a):
@@ -161,51 +248,40 @@ def reference_arm(a):
     if rank != 0:
         return 0
     from oracle import ref
-    from paper_2102_00755_b200 import scenario
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (make -C oracle)"}))
         return 0
-    sample_cfg = a.cpu_sample_config
-    procs = cpu_procs(sample_cfg)
-    sc = scenario.CONFIGS[a.config]()
-    vu_grad = sc.voxel_updates_per_gradient
-    for _ in range(a.warmup):
-        cpu_reference_sample(sample_cfg, 1, procs)
-    rates, times = [], []
-    for _ in range(a.steps):
-        r = cpu_reference_sample(sample_cfg, a.cpu_sample_steps, procs)
-        rates.append(r["rate_aggregate"])
-        times.append(vu_grad / r["rate_aggregate"])
-    value = float(np.median(rates))
-    sample = (f"config {sample_cfg} grid {tuple(scenario.CONFIGS[sample_cfg](nt=2).grid.shape)}: "
-              f"{a.cpu_sample_steps} forward + {a.cpu_sample_steps} adjoint/replay pair steps per process, "
-              f"{procs} concurrent 1-thread processes; FFT = in-repo FFTW-API shim (fp64 Stockham), not FFTW; "
-              f"per-voxel-update rate extrapolated to the {a.config} gradient")
+    g = ref_grid(a.config)
+    n = grid_points(g)
+    vu_grad = n * (3 * int(g.nt) - 3)
+    n_grad = a.batch if a.batch else a.gpus
+    cb = cpu_baseline_block(a.config, vu_grad)
+    value = cb["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "voxel-updates/s",
-        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": float(np.median(times)) * 1e3 / max(1, a.gpus), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(sc, a.gpus),
-        "s_per_gradient_extrapolated": float(np.median(times)),
-        "cpu_baseline": {"value": value, "unit": "voxel-updates/s", "cores": procs, "kind": "reference",
-                         "sample": sample},
+        "n_gpus": a.gpus, "steps": 1, "warmup": 0,
+        "ms_per_step": n_grad * vu_grad / value * 1e3, "higher_is_better": True,
+        "scaling": "strong" if a.batch else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": ref_config_block(a.config, a.gpus, a.batch),
+        "s_per_gradient_extrapolated": vu_grad / value,
+        "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "voxel-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": f"one sample (requested --steps {a.steps} --warmup {a.warmup}): a full reference gradient at this "
+                f"grid takes hours per core, so the per-step rate is measured on the grid and extrapolated",
     }
     print(json.dumps(line))
     return 0
 
 
-def config_block(sc, n_gpus):
+def config_block(sc, n_gpus, batch=0):
     return {"workload": f"config {sc.name}: source-encoded TR c0 gradient, grid {tuple(sc.grid.shape)} "
                         f"(interior {tuple(sc.grid.shape[a] - 2 * sc.grid.pml_size[a] for a in range(3))}), "
                         f"dx {sc.grid.dx[0] * 1e3:g} mm, nt {sc.grid.nt}, {sc.n_src} emitters + "
-                        f"{len(sc.sensors.positions)} receivers, shell thickness {sc.thickness}",
+                        f"{len(sc.sensors.positions)} receivers, shell thickness {sc.thickness}"
+                        + (f", mini-batch of {batch}" if batch else ""),
             "grid": list(sc.grid.shape), "nt": sc.grid.nt, "n_emitters": sc.n_src,
             "n_receivers": len(sc.sensors.positions), "voxel_updates_per_gradient": sc.voxel_updates_per_gradient,
-            "parallelism": f"dp{n_gpus} (one encoded realization per GPU, NCCL mean)" if n_gpus > 1 else "1 GPU",
-            "l2_flush": "inputs larger than L2 (each field >= 126 MB at config D)" if sc.grid.points * 4 > 126e6
-            else "working set may be L2-resident at this size"}
+            "parallelism": parallelism(n_gpus, batch), "l2_flush": l2_note(sc.grid.points)}
 
 
 # ----------------------------------------------------------------------------------------
@@ -234,21 +310,36 @@ def b200_arm(a):
         dist.broadcast_object_list(uid, src=0)
         eng.comm_init(uid[0], world, rank)
 
-    # realization of this rank (weak scaling: one encoded gradient per GPU per step)
-    enc = sc.encoded(rank)
-    # synthetic observed data: forward of the encoded source on the true phantom (setup)
-    eng.set_medium(sc.truth)
-    eng.set_sources(enc)
+    from paper_2102_00755_b200.minibatch import NcclReducer, run_minibatch, shard, slots_per_rank
+    # realizations of this rank: weak scaling = realization `rank` (one encoded gradient per GPU
+    # per step); --batch B = the fixed mini-batch r = rank, rank + W, ... < B (BASELINE config 3)
+    mine = shard(a.batch, world, rank) if a.batch else [rank]
+    batch = a.batch if a.batch else world
+    slots = slots_per_rank(batch, world)
     eng.set_sensors(sc.sensors)
-    observed, _ = eng.forward(0)
+    # synthetic observed data: forward of each encoded source on the true phantom (setup)
+    eng.set_medium(sc.truth)
+    encs, obs = {}, {}
+    for r in mine:
+        encs[r] = sc.encoded(r)
+        eng.set_sources(encs[r])
+        obs[r], _ = eng.forward(0)
     eng.set_medium(sc.model)
-    eng.upload_observed(observed)
+    if len(mine) == 1:
+        eng.set_sources(encs[mine[0]])
+        eng.upload_observed(obs[mine[0]])
+    eng.batch_reserve(slots)
     stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=dev)
 
-    def one_step(accumulate=False):
-        eng.run_gradient(sc.thickness, accumulate=accumulate)
-        if world > 1:
-            eng.allreduce_mean(world)
+    def one_step():
+        # this rank's gradients into its slots, then the deterministic mean over all ranks
+        for r in mine:
+            if len(mine) > 1:
+                eng.set_sources(encs[r])
+                eng.upload_observed(obs[r])
+            eng.run_gradient_slot(sc.thickness, r // world)
+        if world > 1 or batch > 1:
+            eng.batch_mean(batch)
 
     for _ in range(a.warmup):
         one_step()
@@ -275,7 +366,7 @@ def b200_arm(a):
     # per-launch-class CUDA-event timing: one extra gradient with profiling on (the engine
     # then serialises adjoint and replay on one stream so each launch is timed alone)
     eng.set_profiling(True)
-    eng.run_gradient(sc.thickness)
+    eng.run_gradient_slot(sc.thickness, 0)
     stats = eng.kernel_stats()
     prof_ms = sum(v[0] for v in stats.values())
     eng.set_profiling(False)
@@ -286,32 +377,39 @@ def b200_arm(a):
     ms = float(t.item())
     s_per_step = ms / 1e3 / a.steps
     vu = sc.voxel_updates_per_gradient
-    value = world * vu / s_per_step
+    n_grad = batch            # gradients of the whole job per step
+    value = n_grad * vu / s_per_step
 
-    # end to end through the public API: host observed + encoded sources in, gradient out
+    # end to end through the public API: host medium + encoded sources + observed data in,
+    # gradient out (weak: gradient_time_reversal per rank; --batch: the mini-batch driver)
     e2e = None
     if a.e2e_steps > 0:
-        obs_host = np.ascontiguousarray(observed)
         e_times = []
         for _ in range(a.e2e_steps):
             torch.cuda.synchronize(dev)
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            res = E.gradient_time_reversal(sc.model, enc, sc.sensors, obs_host, g, sc.thickness, engine=eng)
-            if world > 1:
-                eng.allreduce_mean(world)
+            if a.batch or world > 1:
+                eng.set_medium(sc.model)
+                run_minibatch(eng, lambda r: encs[r], lambda r: obs[r], sc.thickness, batch, world, rank,
+                              NcclReducer())
+                loss, grad = eng.download_gradient()
+            else:
+                r0 = mine[0]
+                res = E.gradient_time_reversal(sc.model, encs[r0], sc.sensors, obs[r0], g, sc.thickness, engine=eng)
             dt = time.perf_counter() - t0
             tt = torch.tensor([dt], dtype=torch.float64)
             if world > 1:
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e_times.append(float(tt.item()))
         te = float(np.median(e_times))
-        h2d = obs_host.nbytes + enc.weights.nbytes + enc.delays.nbytes + len(enc.positions) * 8 + \
-            sum(np.asarray(s).nbytes for s in enc.signals) + 3 * g.points * 8  # observed, sources, medium (c0, rho0, gamma)
+        h2d = sum(obs[r].nbytes + encs[r].weights.nbytes + encs[r].delays.nbytes + len(encs[r].positions) * 8 +
+                  sum(np.asarray(x).nbytes for x in encs[r].signals) for r in mine) + \
+            3 * g.points * 8  # observed + sources per realization, medium (c0, rho0, gamma)
         d2h = g.points * 8 + 8
-        e2e = {"value": world * vu / te, "unit": "voxel-updates/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "s_per_gradient": te}
+        e2e = {"value": n_grad * vu / te, "unit": "voxel-updates/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "s_per_gradient": te / max(1, len(mine))}
 
     if rank != 0:
         if world > 1:
@@ -346,12 +444,13 @@ def b200_arm(a):
         meas_bytes = None
     line = {
         "metric": METRIC, "value": value, "unit": "voxel-updates/s", "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+        "scaling": "strong" if a.batch else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (breast phantom, golden-spiral bowl, "
                                                      "Rademacher-encoded emitters, observed = forward on truth)",
-        "config": config_block(sc, world),
+        "config": config_block(sc, world, a.batch),
         "voxel_updates_per_s_per_gpu": value / world,
-        "s_per_gradient": s_per_step,
+        "s_per_gradient": s_per_step * world / n_grad,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "peak_kind": peak_kind,
                      "traffic": traffic, "traffic_source": traffic_src,
@@ -375,14 +474,7 @@ def b200_arm(a):
         try:
             from oracle import ref
             if ref.available():
-                procs = cpu_procs(a.cpu_sample_config)
-                r = cpu_reference_sample(a.cpu_sample_config, a.cpu_sample_steps, procs)
-                line["cpu_baseline"] = {
-                    "value": r["rate_aggregate"], "unit": "voxel-updates/s", "cores": procs, "kind": "reference",
-                    "sample": f"reference (oracle/_ref, FFTW-API shim) on config {a.cpu_sample_config} grid: "
-                              f"{a.cpu_sample_steps} fwd + {a.cpu_sample_steps} pair steps x {procs} processes; "
-                              f"per core {r['rate_per_core']:.3g} vu/s; extrapolated s/gradient at "
-                              f"{sc.name}: {vu / r['rate_aggregate']:.4g}"}
+                line["cpu_baseline"] = cpu_baseline_block(a.config, vu)
         except Exception as e:  # baseline is reported, never blocks the bench line
             line["cpu_baseline"] = {"value": None, "unit": "voxel-updates/s", "cores": 0, "kind": "reference",
                                     "sample": f"failed: {e}"}
@@ -402,8 +494,9 @@ def main():
     p.add_argument("--config", default="D", choices=["A", "B", "C", "D"])
     p.add_argument("--e2e-steps", type=int, default=1)
     p.add_argument("--cpu-baseline", type=int, default=1)
-    p.add_argument("--cpu-sample-config", default="B")
-    p.add_argument("--cpu-sample-steps", type=int, default=2)
+    p.add_argument("--batch", type=int, default=0,
+                   help="fixed mini-batch of B encoded realizations sharded over the GPUs (BASELINE config 3); "
+                        "0 = one realization per GPU (weak scaling)")
     p.add_argument("--nt", type=int, default=None, help="override nt (development only; not a valid bench number)")
     a = p.parse_args()
     if a.impl == "reference":

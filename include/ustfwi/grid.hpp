@@ -7,7 +7,8 @@
 #include <stdexcept>
 #include <vector>
 
-#include "ustfwi/core.hpp"
+#include "core.hpp"
+#include "solver.hpp"
 
 namespace ustfwi {
 

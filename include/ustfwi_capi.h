@@ -86,6 +86,10 @@ USTFWI_API int ustfwi_ball_mask(int ndim, const int* dims, const double* center,
 /* synth_source_pulse (solver/simulate.hpp:124-148); same two-call protocol via *len. */
 USTFWI_API int ustfwi_synth_source_pulse(const ustfwi_grid* grid, double center_freq_fraction, double c0_min,
                               double* out, int* len);
+/* design_kaiser_lowpass (grid/filter.hpp:38-66): odd-length Kaiser FIR taps with unit DC gain;
+ * two-call protocol via *len (out == NULL queries the length). */
+USTFWI_API int ustfwi_design_kaiser_lowpass(double dt, double cutoff_hz, double transition, double atten_db,
+                                            double* out, int* len);
 /* Encoding realization (SPEC.md stochastic_estimators, EncodingRealization :277-280, RNG
  * contract :331-334): Rademacher weights w_i in {-1,+1} and delays d_i ~ U[0,1] quantized to
  * delay_steps_i = round(d_i * tau / dt), from a counter-based stream keyed by
@@ -93,6 +97,12 @@ USTFWI_API int ustfwi_synth_source_pulse(const ustfwi_grid* grid, double center_
 USTFWI_API int ustfwi_draw_realization(size_t n_src, double tau, double dt, uint64_t master_seed,
                             uint64_t iteration, uint64_t index, int8_t* weights,
                             int32_t* delay_steps, double* delays_unit);
+
+/* fp64 host FFT over interleaved complex data [dims] (row-major): the reference's
+ * ComplexFft (core/fft.hpp:75-118; FFTW conventions: forward e^{-i}, unnormalised; inverse
+ * e^{+i}, scaled by 1/N when normalize != 0). Serves the fp64 setup utilities of the drop-in
+ * headers (spectral_derivative, fourier_shift, RealFft); never the device hot path. */
+USTFWI_API int ustfwi_host_fft(int ndim, const int* dims, double* data, int inverse, int normalize);
 
 /* ------------------------------------------------------------------------------------
  * Device engine
@@ -162,6 +172,33 @@ USTFWI_API int ustfwi_gpu_evaluate_loss(ustfwi_gpu_ctx* ctx, const double* obser
  * by stagger (USTFWI_STAGGER_*). Test/diagnostic entry of the K1 passes. */
 USTFWI_API int ustfwi_gpu_derivative(ustfwi_gpu_ctx* ctx, const double* f, int axis, int stagger,
                           double* out);
+
+/* SpectralEngine::half_shift (engine.hpp:131-137): band-limited shift by direction * dx/2
+ * along axis (the Nyquist bin keeps its real part). */
+USTFWI_API int ustfwi_gpu_half_shift(ustfwi_gpu_ctx* ctx, const double* f, int axis, int direction, double* out);
+
+/* ---- WaveStepper, step by step (solver/engine.hpp:170-386) ----
+ * A context hosts two steppers (which = 0, 1) on its bound medium. init = the constructor with
+ * StepperOptions {pml_enabled, absorption_sign, dispersion_enabled} (:170-177,184-259) and a
+ * zero state; update_velocity_density (:270-292); inject = inject_mass_source for n positions
+ * applied in order (:296-300); enforce = enforce_shell with density values (:304-307);
+ * refresh_pressure = refresh_pressure_from_density (:311-316); update_pressure (:318-347; a
+ * NumericalError every 64th step when p[0] is not finite); read = pressure() / velocity()[a] /
+ * the split densities as fp64 (field 0 p, 1..ndim v_a, 4..3+ndim rho_a); gather = p at n
+ * positions. The hot path (forward / gradient) never goes through these calls. */
+USTFWI_API int ustfwi_gpu_stepper_init(ustfwi_gpu_ctx* ctx, int which, int pml_enabled, double absorption_sign,
+                                       int dispersion_enabled);
+USTFWI_API int ustfwi_gpu_stepper_reset(ustfwi_gpu_ctx* ctx, int which);
+USTFWI_API int ustfwi_gpu_stepper_update_velocity_density(ustfwi_gpu_ctx* ctx, int which);
+USTFWI_API int ustfwi_gpu_stepper_inject(ustfwi_gpu_ctx* ctx, int which, size_t n, const size_t* idx,
+                                         const double* amplitude);
+USTFWI_API int ustfwi_gpu_stepper_enforce(ustfwi_gpu_ctx* ctx, int which, size_t n, const size_t* idx,
+                                          const double* values);
+USTFWI_API int ustfwi_gpu_stepper_refresh_pressure(ustfwi_gpu_ctx* ctx, int which);
+USTFWI_API int ustfwi_gpu_stepper_update_pressure(ustfwi_gpu_ctx* ctx, int which);
+USTFWI_API int ustfwi_gpu_stepper_read(ustfwi_gpu_ctx* ctx, int which, int field, double* out);
+USTFWI_API int ustfwi_gpu_stepper_gather(ustfwi_gpu_ctx* ctx, int which, size_t n, const size_t* idx, double* out);
+USTFWI_API int ustfwi_gpu_stepper_step_index(ustfwi_gpu_ctx* ctx, int which, int* out);
 
 /* ---- device-resident variants (inputs already in HBM; used by the benchmark and by the
  *      multi-GPU mini-batch driver) ---- */

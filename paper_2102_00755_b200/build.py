@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libustfwi_b200.so")
-SOURCES = ["engine.cu", "kernels.cu", "passes.cu", "passes_y.cu", "lbfgs.cu", "resample.cu", "host_setup.cpp"]
+SOURCES = ["engine.cu", "kernels.cu", "passes.cu", "passes_y.cu", "lbfgs.cu", "resample.cu", "host_setup.cpp", "host_fft.cpp"]
 HEADERS = ["passes.cu", "fft_smem.cuh", "fft_reg.cuh", "async_copy.cuh", "kernels.cuh", "host_setup.hpp", os.path.join("..", "..", "include", "ustfwi_capi.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -30,7 +30,11 @@ EXPORTS = [
     "ustfwi_gpu_upload_observed", "ustfwi_gpu_run_gradient", "ustfwi_gpu_download_gradient",
     "ustfwi_gpu_accumulator", "ustfwi_gpu_synchronize", "ustfwi_gpu_stream", "ustfwi_gpu_launch_count",
     "ustfwi_gpu_shell_size", "ustfwi_gpu_set_profiling", "ustfwi_gpu_kernel_stats", "ustfwi_nccl_unique_id", "ustfwi_gpu_comm_init",
-    "ustfwi_gpu_batch_reserve", "ustfwi_gpu_run_gradient_slot", "ustfwi_gpu_batch_mean", "ustfwi_gpu_set_nt",
+    "ustfwi_gpu_batch_reserve", "ustfwi_gpu_run_gradient_slot", "ustfwi_gpu_batch_mean", "ustfwi_gpu_set_nt", "ustfwi_host_fft", "ustfwi_design_kaiser_lowpass", "ustfwi_gpu_half_shift",
+    "ustfwi_gpu_stepper_init", "ustfwi_gpu_stepper_reset", "ustfwi_gpu_stepper_update_velocity_density",
+    "ustfwi_gpu_stepper_inject", "ustfwi_gpu_stepper_enforce", "ustfwi_gpu_stepper_refresh_pressure",
+    "ustfwi_gpu_stepper_update_pressure", "ustfwi_gpu_stepper_read", "ustfwi_gpu_stepper_gather",
+    "ustfwi_gpu_stepper_step_index",
     "ustfwi_lbfgs_create", "ustfwi_lbfgs_destroy", "ustfwi_lbfgs_reset", "ustfwi_lbfgs_push", "ustfwi_lbfgs_apply",
     "ustfwi_lbfgs_pairs", "ustfwi_fourier_interpolate", "ustfwi_lowpass_timeseries", "ustfwi_restrict_traces",
 ]

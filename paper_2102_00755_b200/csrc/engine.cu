@@ -39,6 +39,15 @@ struct Sim {
     float* v[3] = {};
     float* rho[3] = {};
     float2* S[3] = {};
+    bool pml_off = false;   // StepperOptions::pml_enabled == false (engine.hpp:171,202-213)
+};
+
+// WaveStepper options and counters of the step-level C ABI (engine.hpp:170-177,344-346)
+struct StepperState {
+    bool init = false;
+    float abs_sign = 1.f;
+    bool dispersion = true;
+    int step_index = 0;
 };
 
 // Device image of a SourceSet: unique positions (sorted) + CSR of contributions.
@@ -120,6 +129,12 @@ struct ustfwi_gpu_ctx {
     float2* dmul[3][ST_COUNT] = {};  // per padded axis: none / plus / minus / shift +1/2 / shift -1/2 tables
     float* pml_reg[3] = {};
     float* pml_stag[3] = {};
+    float* pml_one[3] = {};   // all-ones profiles (PML disabled)
+    StepperState stp[2];
+    float* stp_scratch = nullptr;   // pressure output of a density-only step
+    int* stp_idx = nullptr;         // staging of the sparse step-level calls
+    float* stp_val = nullptr;
+    size_t stp_cap = 0;
 
     // medium
     bool has_medium = false;
@@ -343,6 +358,7 @@ struct StepIO {
     int step_n = 0;
     int check_step = 0;
     float* p_out = nullptr;
+    bool density_only = false;            // stop after the density update (WaveStepper API)
     cudaEvent_t wait_before_z = nullptr;  // cross-stream dependency of the pressure kernel
     // absorbing media
     float abs_sign = 1.f;                 // absorption_sign (-1 in the time-reversal replay)
@@ -447,7 +463,9 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     j.job[0] = {0, 0, c.dmul[0][ST_PLUS], 1};
     j.job[1] = {0, 1, nullptr, 1};
     pencil(g, 1.0, 0, false, j);
-    Pml ps{{c.pml_stag[0], c.pml_stag[1], c.pml_stag[2]}};
+    float* const* stag = s.pml_off ? c.pml_one : c.pml_stag;
+    float* const* regp = s.pml_off ? c.pml_one : c.pml_reg;
+    Pml ps{{stag[0], stag[1], stag[2]}};
     const double coef_b = c.dtr_stag[0].field ? 3 * FB : 0.0;
     chunked([&](const GridDev& gc, double frac) {
         PencilJobs jj{};
@@ -478,7 +496,7 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
         a.rho[f] = s.rho[f];
     }
     a.dz_minus = c.dmul[2][ST_MINUS];
-    a.pml = Pml{{c.pml_reg[0], c.pml_reg[1], c.pml_reg[2]}};
+    a.pml = Pml{{regp[0], regp[1], regp[2]}};
     a.dtrho0 = c.dtrho0;
     a.c0sq = c.c0sq;
     a.p_out = io.p_out;
@@ -518,13 +536,13 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
         pencil(gc, frac, 1, true, jj);
         c.launch(KIND_ZRHO, frac * zb, [&] { return launch_zrho(gc, a, true, st); }, st);
         if (split) ++c.launches;
-        if (c.absorbing) return;
+        if (c.absorbing || io.density_only) return;
         // Y forward of Fz p for the next step
         jj.n = 1;
         jj.job[0] = {0, 0, nullptr, 0};
         pencil(gc, frac, 1, false, jj);
     });
-    if (c.absorbing) absorbing_tail(c, s, io, st);
+    if (c.absorbing && !io.density_only) absorbing_tail(c, s, io, st);
 }
 
 // Y forward of S0 (after a pressure refresh outside run_step): restores the run_step
@@ -1173,6 +1191,7 @@ int ustfwi_gpu_create(int device, const ustfwi_grid* grid, ustfwi_gpu_ctx** out)
             }
             c->pml_reg[a] = c->upload(std::vector<float>(r.begin(), r.end()));
             c->pml_stag[a] = c->upload(std::vector<float>(st.begin(), st.end()));
+            c->pml_one[a] = c->upload(std::vector<float>(static_cast<size_t>(n), 1.f));
         }
         g.kx = kdev[0];
         g.ky = kdev[1];
@@ -1528,6 +1547,196 @@ int ustfwi_gpu_evaluate_loss(ustfwi_gpu_ctx* c, const double* observed, double* 
                 loss = t;
             }
         *loss_out = loss;
+    });
+}
+
+// ---- WaveStepper on the device (solver/engine.hpp:170-386), step by step ----------------
+
+namespace {
+Sim& stepper_sim(Ctx& c, int which) {
+    if (which < 0 || which > 1) fail(USTFWI_ERR_INVALID, "stepper index must be 0 or 1");
+    if (!c.stp[which].init) fail(USTFWI_ERR_INVALID, "stepper not initialised (ustfwi_gpu_stepper_init)");
+    return c.sim[which];
+}
+void stage_sparse(Ctx& c, size_t n, const size_t* idx, const std::vector<float>& val) {
+    if (n > c.stp_cap) {
+        c.release(c.stp_idx);
+        c.release(c.stp_val);
+        c.stp_idx = c.alloc<int>(n);
+        c.stp_val = c.alloc<float>(n);
+        c.stp_cap = n;
+    }
+    std::vector<int> ii(n);
+    for (size_t i = 0; i < n; ++i) {
+        if (idx[i] >= static_cast<size_t>(c.g.N)) fail(USTFWI_ERR_INVALID, "position outside grid");
+        ii[i] = static_cast<int>(idx[i]);
+    }
+    CK(cudaMemcpyAsync(c.stp_idx, ii.data(), n * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    CK(cudaMemcpyAsync(c.stp_val, val.data(), n * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+}
+// p = c0^2 sum_a rho_a and the entry invariant S0 = Fy Fz p of the next step
+void stepper_pressure(Ctx& c, Sim& s, int check_step) {
+    ZrhoArgs a{};
+    for (int f = 0; f < 3; ++f) {
+        a.S[f] = s.S[f];
+        a.rho[f] = s.rho[f];
+    }
+    a.pml = Pml{{c.pml_reg[0], c.pml_reg[1], c.pml_reg[2]}};
+    a.dtrho0 = c.dtrho0;
+    a.c0sq = c.c0sq;
+    a.p_out = s.p;
+    a.a_first = c.off_axis;
+    a.check_step = check_step;
+    a.diverged = c.flags;
+    c.count(launch_zrho(c.g, a, false, c.stream));
+    y_forward_p(c, s, c.stream);
+}
+}  // namespace
+
+int ustfwi_gpu_stepper_init(ustfwi_gpu_ctx* c, int which, int pml_enabled, double absorption_sign,
+                            int dispersion_enabled) {
+    return guarded(c, [&] {
+        if (which < 0 || which > 1) fail(USTFWI_ERR_INVALID, "stepper index must be 0 or 1");
+        require_medium(*c);
+        Sim& s = c->sim[which];
+        if (!s.p) s.p = c->alloc<float>(static_cast<size_t>(c->g.N));
+        if (!c->stp_scratch) c->stp_scratch = c->alloc<float>(static_cast<size_t>(c->g.N));
+        s.pml_off = pml_enabled == 0;
+        StepperState& t = c->stp[which];
+        t.init = true;
+        t.abs_sign = static_cast<float>(absorption_sign);
+        t.dispersion = dispersion_enabled != 0;
+        t.step_index = 0;
+        reset_sim(*c, s, true);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ustfwi_gpu_stepper_reset(ustfwi_gpu_ctx* c, int which) {
+    return guarded(c, [&] {
+        Sim& s = stepper_sim(*c, which);
+        reset_sim(*c, s, true);
+        c->stp[which].step_index = 0;
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ustfwi_gpu_stepper_update_velocity_density(ustfwi_gpu_ctx* c, int which) {
+    return guarded(c, [&] {
+        Sim& s = stepper_sim(*c, which);
+        c->disp_active = c->dispersion && c->stp[which].dispersion;
+        StepIO io;
+        io.density_only = true;
+        io.p_out = c->stp_scratch;
+        run_step(*c, s, io, c->stream);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ustfwi_gpu_stepper_inject(ustfwi_gpu_ctx* c, int which, size_t n, const size_t* idx, const double* amp) {
+    return guarded(c, [&] {
+        Sim& s = stepper_sim(*c, which);
+        std::vector<float> v(n);
+        for (size_t i = 0; i < n; ++i) {
+            if (idx[i] >= static_cast<size_t>(c->g.N)) fail(USTFWI_ERR_INVALID, "source position outside grid");
+            const double c0 = c->c0_host[idx[i]];
+            v[i] = static_cast<float>(amp[i] * (2.0 * c->grid.dt / (c->ndim * c->grid.dx[0] * std::sqrt(c0 * c0))));
+        }
+        stage_sparse(*c, n, idx, v);
+        c->count(launch_stepper_sparse(s.rho, c->off_axis, c->stp_idx, c->stp_val, static_cast<int>(n), 0, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ustfwi_gpu_stepper_enforce(ustfwi_gpu_ctx* c, int which, size_t n, const size_t* idx, const double* values) {
+    return guarded(c, [&] {
+        Sim& s = stepper_sim(*c, which);
+        const auto v = to_f32(values, n);
+        stage_sparse(*c, n, idx, v);
+        c->count(launch_stepper_sparse(s.rho, c->off_axis, c->stp_idx, c->stp_val, static_cast<int>(n), 1, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ustfwi_gpu_stepper_refresh_pressure(ustfwi_gpu_ctx* c, int which) {
+    return guarded(c, [&] {
+        Sim& s = stepper_sim(*c, which);
+        stepper_pressure(*c, s, 0);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ustfwi_gpu_stepper_update_pressure(ustfwi_gpu_ctx* c, int which) {
+    return guarded(c, [&] {
+        Sim& s = stepper_sim(*c, which);
+        StepperState& t = c->stp[which];
+        const int k = ++t.step_index;
+        const int check = (k & 63) == 0 ? k : 0;
+        if (check) clear_flags(*c);
+        if (c->absorbing) {
+            c->disp_active = c->dispersion && t.dispersion;
+            StepIO io;
+            io.p_out = s.p;
+            io.abs_sign = t.abs_sign;
+            io.check_step = check;
+            absorbing_tail(*c, s, io, c->stream);
+        } else {
+            stepper_pressure(*c, s, check);
+        }
+        if (check) check_flags(*c, false);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ustfwi_gpu_stepper_read(ustfwi_gpu_ctx* c, int which, int field, double* out) {
+    return guarded(c, [&] {
+        Sim& s = stepper_sim(*c, which);
+        const float* src = nullptr;
+        if (field == 0) src = s.p;
+        else if (field >= 1 && field <= c->ndim) src = s.v[field - 1 + c->off_axis];
+        else if (field >= 4 && field <= 3 + c->ndim) src = s.rho[field - 4 + c->off_axis];
+        else fail(USTFWI_ERR_INVALID, "field must be 0 (p), 1..ndim (v_a) or 4..3+ndim (rho_a)");
+        const size_t N = static_cast<size_t>(c->g.N);
+        std::vector<float> h(N);
+        CK(cudaMemcpyAsync(h.data(), src, N * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (size_t i = 0; i < N; ++i) out[i] = h[i];
+    });
+}
+
+int ustfwi_gpu_stepper_gather(ustfwi_gpu_ctx* c, int which, size_t n, const size_t* idx, double* out) {
+    return guarded(c, [&] {
+        Sim& s = stepper_sim(*c, which);
+        if (n == 0) return;
+        stage_sparse(*c, n, idx, std::vector<float>(n, 0.f));
+        c->count(launch_pick(s.p, c->stp_idx, static_cast<int>(n), c->stp_val, c->stream));
+        std::vector<float> h(n);
+        CK(cudaMemcpyAsync(h.data(), c->stp_val, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (size_t i = 0; i < n; ++i) out[i] = h[i];
+    });
+}
+
+int ustfwi_gpu_stepper_step_index(ustfwi_gpu_ctx* c, int which, int* out) {
+    return guarded(c, [&] {
+        stepper_sim(*c, which);
+        *out = c->stp[which].step_index;
+    });
+}
+
+int ustfwi_gpu_half_shift(ustfwi_gpu_ctx* c, const double* f, int axis, int direction, double* out) {
+    return guarded(c, [&] {
+        if (axis < 0 || axis >= c->ndim) fail(USTFWI_ERR_INVALID, "axis out of range");
+        const size_t N = static_cast<size_t>(c->g.N);
+        const int pa = axis + c->off_axis;
+        const auto h = to_f32(f, N);
+        CK(cudaMemcpyAsync(c->ring[0], h.data(), N * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        spectral_apply(*c, c->sim[1], c->ring[0], pa, c->dmul[pa][direction > 0 ? ST_SHIFT : ST_SHIFTM], 0, c->ring[1],
+                       c->stream);
+        std::vector<float> o(N);
+        CK(cudaMemcpyAsync(o.data(), c->ring[1], N * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (size_t i = 0; i < N; ++i) out[i] = o[i];
     });
 }
 

@@ -348,6 +348,16 @@ int ustfwi_synth_source_pulse(const ustfwi_grid* grid, double frac, double c0_mi
     });
 }
 
+int ustfwi_design_kaiser_lowpass(double dt, double cutoff_hz, double transition, double atten_db, double* out,
+                                 int* len) {
+    return guarded([&] {
+        if (!len) fail(USTFWI_ERR_INVALID, "null length");
+        const auto h = kaiser_lowpass(dt, cutoff_hz, transition, atten_db);
+        if (out) std::copy(h.begin(), h.begin() + std::min<long>(static_cast<long>(h.size()), *len), out);
+        *len = static_cast<int>(h.size());
+    });
+}
+
 int ustfwi_draw_realization(size_t n_src, double tau, double dt, uint64_t master_seed, uint64_t iteration,
                             uint64_t index, int8_t* weights, int32_t* delay_steps, double* delays_unit) {
     return guarded([&] {

@@ -682,6 +682,38 @@ cudaError_t launch_ordered_mean(long long n, const float* gathered, int world, i
     return cudaGetLastError();
 }
 
+// WaveStepper::inject_mass_source / enforce_shell (engine.hpp:296-307) for the step-level C
+// ABI: one thread applies the list in order (mode 0: rho_a[idx] += val, mode 1: rho_a[idx] =
+// val for every active axis a), so repeated positions behave as the reference's loop.
+__global__ void stepper_sparse_kernel(float* r0, float* r1, float* r2, int a_first, const int* __restrict__ idx,
+                                      const float* __restrict__ val, int n, int mode) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    float* r[3] = {r0, r1, r2};
+    for (int i = 0; i < n; ++i)
+        for (int a = a_first; a < 3; ++a) {
+            if (mode == 0) r[a][idx[i]] += val[i];
+            else r[a][idx[i]] = val[i];
+        }
+}
+
+__global__ void pick_kernel(const float* __restrict__ f, const int* __restrict__ idx, int n, float* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = f[idx[i]];
+}
+
+cudaError_t launch_stepper_sparse(float* const rho[3], int a_first, const int* idx, const float* val, int n, int mode,
+                                  cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    stepper_sparse_kernel<<<1, 1, 0, st>>>(rho[0], rho[1], rho[2], a_first, idx, val, n, mode);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pick(const float* f, const int* idx, int n, float* out, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    pick_kernel<<<(n + 255) / 256, 256, 0, st>>>(f, idx, n, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gather(const float* p, const SparseGather& g, cudaStream_t st) {
     if (g.n <= 0) return cudaSuccess;
     gather_kernel<<<(g.n + 255) / 256, 256, 0, st>>>(p, g);

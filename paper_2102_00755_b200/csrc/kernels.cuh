@@ -248,6 +248,9 @@ cudaError_t launch_abs_pressure(long long n, const AbsArgs& a, cudaStream_t st);
 cudaError_t launch_correlate(long long n, const float* p_new, const float* c0sq, const Correlate& c, cudaStream_t st);
 cudaError_t launch_gather(const float* p, const SparseGather& g, cudaStream_t st);
 cudaError_t launch_rho0_elem(long long n, int mode, const Rho0Args& a, cudaStream_t st);
+cudaError_t launch_stepper_sparse(float* const rho[3], int a_first, const int* idx, const float* val, int n, int mode,
+                                  cudaStream_t st);
+cudaError_t launch_pick(const float* f, const int* idx, int n, float* out, cudaStream_t st);
 cudaError_t launch_ordered_mean(long long n, const float* gathered, int world, int slots, int batch, float* out,
                                 cudaStream_t st);
 

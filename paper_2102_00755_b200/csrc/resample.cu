@@ -260,7 +260,9 @@ void lowpass_dev(Pool& pool, const float* in, float* out, long long n_series, in
 template <class Fn>
 int rguard(int device, Fn&& fn) {
     try {
-        RCK(cudaSetDevice(device));
+        // argument checks run before the device is touched (std::invalid_argument semantics
+        // hold without a GPU); the bodies select the device with use_device()
+        (void)device;
         fn();
         return USTFWI_OK;
     } catch (const Fail& f) {
@@ -297,6 +299,7 @@ USTFWI_API int ustfwi_fourier_interpolate(int device, int ndim, const int* dims,
                 throw Fail{USTFWI_ERR_INVALID, "target dims must be even and >= 4"};
             if (dims[a] % 2 != 0) throw Fail{USTFWI_ERR_INVALID, "source dims must be even"};
         }
+        RCK(cudaSetDevice(device));
         Stream st;
         Pool pool;
         std::vector<long long> cur(dims, dims + ndim);
@@ -335,7 +338,10 @@ USTFWI_API int ustfwi_fourier_interpolate(int device, int ndim, const int* dims,
 USTFWI_API int ustfwi_lowpass_timeseries(int device, size_t n_series, size_t len, const double* sig, double dt,
                                          double cutoff_hz, double transition, double atten_db, double* out) {
     return rguard(device, [&] {
+        if (!(cutoff_hz > 0.0) || cutoff_hz > 0.5 / dt)
+            throw Fail{USTFWI_ERR_INVALID, "cutoff must lie in (0, Nyquist]"};
         if (len == 0 || n_series == 0) return;
+        RCK(cudaSetDevice(device));
         Stream st;
         Pool pool;
         const size_t n = n_series * len;
@@ -364,17 +370,22 @@ USTFWI_API int ustfwi_restrict_traces(int device, size_t n_series, size_t nt, co
             std::copy(data, data + n_series * nt, out);
             return;
         }
+        RCK(cudaSetDevice(device));
         Stream st;
         Pool pool;
-        const size_t n = n_series * nt, nc = n_series * ntc;
-        std::vector<float> h(std::max(n, nc));
-        for (size_t i = 0; i < n; ++i) h[i] = static_cast<float>(data[i]);
+        // zero-pad every trace to ntc * eta samples so that the Fourier resampling to ntc
+        // points keeps the coarse spacing exactly eta * dt_fine (nt need not divide by eta)
+        const size_t ntp = ntc * static_cast<size_t>(eta);
+        const size_t n = n_series * ntp, nc = n_series * ntc;
+        std::vector<float> h(std::max(n, nc), 0.f);
+        for (size_t s = 0; s < n_series; ++s)
+            for (size_t i = 0; i < nt; ++i) h[s * ntp + i] = static_cast<float>(data[s * nt + i]);
         float* a = pool.alloc<float>(n);
         float* b = pool.alloc<float>(nc);
         float* c = pool.alloc<float>(nc);
         RCK(cudaMemcpyAsync(a, h.data(), n * sizeof(float), cudaMemcpyHostToDevice, st.s));
         // Fourier resampling of each trace to the coarse sampling, then the Kaiser low-pass
-        resample_axis(pool, a, b, {static_cast<long long>(n_series), static_cast<long long>(nt)}, 1,
+        resample_axis(pool, a, b, {static_cast<long long>(n_series), static_cast<long long>(ntp)}, 1,
                       static_cast<int>(ntc), false, st.s);
         lowpass_dev(pool, b, c, static_cast<long long>(n_series), static_cast<int>(ntc), dt_fine * eta, cutoff_hz,
                     0.1, 60.0, st.s);

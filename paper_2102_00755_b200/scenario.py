@@ -217,13 +217,15 @@ def config_e(level: int, nt=None):
                            nt if nt is not None else nt_paper)
 
 
-def encoding_problem(n_src: int):
+def encoding_problem(n_src: int, nt: Optional[int] = None):
     """Small 3-D source-encoding problem (24^3 interior -> 64^3, up to 4 emitters, 6 receivers,
     ball gamma r = 8, Gaussian c0 bump): the inputs of the delayed / unbiasedness parity
     fixtures (tests/golden/make_golden_delayed.py) and tests/test_gpu_encoding.py.
     Returns (grid, model, truth, emitter positions, receiver positions, pulse)."""
     interior, dx = [24, 24, 24], 1e-3
     g = capi.make_grid(interior, dx, C0_MAX, 2 * interior[0] * dx / C0_MIN)
+    if nt is not None:
+        g.nt = int(nt)
     shape = g.shape
     c = [s // 2 for s in shape]
     gamma = capi.ball_mask(shape, c, 8.0)

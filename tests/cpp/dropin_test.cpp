@@ -90,13 +90,25 @@ int main() {
         SensorData zero = obs;
         auto ga = gradient_time_reversal(m, s1, sensors, zero, g, 4, GradientParam::alpha0, &eng);
         EXPECT(ga.loss > 0.0 && max_abs(ga.grad) > 0.0);
-        bool rho_threw = false;
+        // rho0 gradient (GradientParam::rho0, gradient.hpp:117-128,213-239)
+        auto gr0 = gradient_time_reversal(m, s1, sensors, zero, g, 4, GradientParam::rho0, &eng);
+        EXPECT(gr0.loss > 0.0 && max_abs(gr0.grad) > 0.0);
+        // GradientOptions default method is full_storage (gradient.hpp:23): rejected, never
+        // silently replaced; gradient_full_storage (gradient.hpp:466-476) throws the same way
+        bool fs_threw = false;
         try {
-            gradient_time_reversal(m, s1, sensors, zero, g, 4, GradientParam::rho0, &eng);
+            compute_gradient(m, s1, sensors, zero, g, GradientParam::c0, GradientOptions{}, &eng);
         } catch (const std::invalid_argument&) {
-            rho_threw = true;
+            fs_threw = true;
         }
-        EXPECT(rho_threw);
+        EXPECT(fs_threw);
+        fs_threw = false;
+        try {
+            gradient_full_storage(m, s1, sensors, zero, g, GradientParam::c0, 1, &eng);
+        } catch (const std::invalid_argument&) {
+            fs_threw = true;
+        }
+        EXPECT(fs_threw);
     }
     // multigrid transfer (grid/spectral.hpp, grid/filter.hpp): up-down round trip, DC gain
     {

@@ -6,11 +6,11 @@ no encoding code, so the oracle runs its own compute_gradient
 EXPANDED SourceSet (each delayed signal with d_i tau / dt zeros prepended, weights folded in)
 over the extended grid — the exact inputs the device path builds on the fly.
 
-    python tests/golden/make_golden_delayed.py      (~15 min single-threaded)
+    python tests/golden/make_golden_delayed.py      (~50 min single-threaded)
 
 delayed_encoding.npz
   small 3-D problem (scenario.encoding_problem: 24^3 interior -> 64^3, 2 emitters, 6 receivers, ball gamma r = 8):
-  * per-source observed data f_i (truth medium), nt
+  * per-source observed data f_i (truth medium), nt = 768 (every field has left the domain)
   * the tau = 2T, d = (0, 1), w = (+1, -1) encoded gradient and loss over nt_ext = 3 nt
     (the second emitter fires after the first's field has left the domain)
   * the exact 2-source gradient sum_i grad D_i and loss sum_i D_i (SPEC.md:304 bar 1e-3)
@@ -36,8 +36,13 @@ from paper_2102_00755_b200.engine import Medium  # noqa: E402
 OUT = os.path.dirname(os.path.abspath(__file__))
 
 
-def small_problem(n_src):
-    return scenario.encoding_problem(n_src)
+# The tau = 2T check needs every single-source field to have left the domain within T: the
+# pulse (peak near sample 200, ~400 samples long) plus one domain crossing (~260 steps) -> nt 768
+DELAYED_NT = 768
+
+
+def small_problem(n_src, nt=None):
+    return scenario.encoding_problem(n_src, nt)
 
 
 def with_nt(g, nt):
@@ -47,7 +52,7 @@ def with_nt(g, nt):
 
 
 def delayed_fixture():
-    g, model, truth, srcs, sens, pulse = small_problem(2)
+    g, model, truth, srcs, sens, pulse = small_problem(2, DELAYED_NT)
     nt = g.nt
     t0 = time.time()
     f = [ref.simulate_forward(g, truth, [s], [pulse], sens)[0] for s in srcs]

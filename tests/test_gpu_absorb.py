@@ -105,8 +105,10 @@ def test_alpha0_and_y_gradients(setup, param, key, lossless):
     assert rel(grad.ravel()[z["gamma_idx"]], z[key]) < GRAD_TOL
 
 
-def test_rho0_gradient_is_rejected(setup):
+def test_rho0_gradient_is_computed(setup):
+    # GradientParam::rho0 (gradient.hpp:117-128,213-239); parity against the reference is in
+    # tests/test_gpu_encoding.py::test_rho0_gradient_matches_reference
     sc, z, eng = setup
     eng.set_medium(sc.model)
-    with pytest.raises(ValueError, match="rho0"):
-        eng.gradient_tr(np.zeros((len(sc.sensors.positions), int(z["nt"]))), 8, param="rho0")
+    loss, grad = eng.gradient_tr(np.zeros((len(sc.sensors.positions), int(z["nt"]))), 8, param="rho0")
+    assert loss > 0 and np.isfinite(grad).all() and np.abs(grad).max() > 0

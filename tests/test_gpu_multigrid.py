@@ -59,3 +59,17 @@ def test_restrict_data_properties():
         assert r.shape == (2, 401)
         mid = r[:, 120:-120]  # beyond the 183-tap Kaiser filter's reach into the zero padding
         assert np.allclose(mid, 0.75 * scale, rtol=1e-5)
+
+
+def test_restrict_data_odd_nt_keeps_arrival_time():
+    # with nt % eta != 0 the coarse spacing must stay eta * dt_fine (traces are
+    # zero-padded to ceil(nt/eta) * eta before resampling): a band-limited pulse centred at
+    # fine sample 250 of a 301-sample trace lands at coarse sample 125 (eta = 2)
+    dt = 1e-7
+    t = np.arange(301)
+    pulse = np.exp(-0.5 * ((t - 250.0) / 6.0) ** 2)[None, :]
+    r = multigrid.restrict_data(pulse, 2, 3, dt, 1.5e6)[0]
+    k = int(np.argmax(r))
+    y0, y1, y2 = r[k - 1], r[k], r[k + 1]
+    peak = k + 0.5 * (y0 - y2) / (y0 - 2 * y1 + y2)   # parabolic refinement
+    assert abs(peak - 125.0) < 0.05, peak
