@@ -212,6 +212,27 @@ struct ustfwi_gpu_ctx {
 
     void* comm = nullptr;
     int nranks = 1, rank = 0;
+    // CUDA graph of the gradient's device work, valid while nothing was re-bound (epoch)
+    uint64_t epoch = 1;
+    struct GraphKey {
+        uint64_t epoch = 0;
+        int thickness = 0;
+        bool accumulate = false;
+        bool operator==(const GraphKey& o) const {
+            return epoch == o.epoch && thickness == o.thickness && accumulate == o.accumulate;
+        }
+    };
+    GraphKey grad_key{}, seen_key{};
+    cudaGraphExec_t grad_graph = nullptr;
+    uint64_t grad_graph_launches = 0;
+    void drop_graph() {
+        if (grad_graph) cudaGraphExecDestroy(grad_graph);
+        grad_graph = nullptr;
+    }
+    void touch() {
+        ++epoch;
+        drop_graph();
+    }
     // mini-batch slots (ustfwi_gpu_run_gradient_slot / ustfwi_gpu_batch_mean): per-realization
     // masked gradients and losses of this rank, and the all-gathered copy of every rank's
     int n_slots = 0;
@@ -638,6 +659,7 @@ void ensure_data_buffers(Ctx& c) {
 // the sensors or the simulation length change (ustfwi_gpu_set_nt: the encoded duration
 // T + tau of a delayed realization).
 void rebind_time_buffers(Ctx& c) {
+    c.touch();
     for (void* q : {(void*)c.data, (void*)c.obs, (void*)c.q, (void*)c.loss_part}) c.release(q);
     c.data = nullptr;
     c.obs_ready = false;
@@ -652,6 +674,7 @@ void rebind_time_buffers(Ctx& c) {
 void prepare_shell(Ctx& c, int thickness) {
     if (c.gamma_host.empty()) fail(USTFWI_ERR_INVALID, "boundary recording requires a gamma mask");
     if (thickness != c.shell_thickness || !c.shell_pos) {
+        c.touch();
         c.release(c.shell_pos);
         c.shell_pos = nullptr;
         std::vector<int> dims(c.grid.dims, c.grid.dims + c.grid.ndim);
@@ -664,6 +687,7 @@ void prepare_shell(Ctx& c, int thickness) {
     }
     const size_t need = c.shell_host.size() * static_cast<size_t>(c.grid.nt);
     if (need > c.trace_elems) {
+        c.touch();
         c.release(c.trace);
         c.trace = c.alloc<float>(need);
         c.trace_elems = need;
@@ -687,13 +711,18 @@ void check_flags(Ctx& c, bool grad_phase) {
 
 // simulate_forward (simulate.hpp:76-103): nt steps of stepper 0 with the source set,
 // sensor gather into c.data ([nt][ns]) and optional shell record into c.trace.
-void forward_sim(Ctx& c, int thickness) {
+void forward_prep(Ctx& c, int thickness) {
     require_medium(c);
     ensure_data_buffers(c);
     if (thickness > 0) prepare_shell(c, thickness);
     refresh_scales(c, c.src);
+}
+
+// the launches of the forward simulation only (no host transfers: capturable)
+void forward_steps(Ctx& c, int thickness) {
     c.disp_active = c.dispersion;  // simulate_forward: default StepperOptions
     Sim& s = c.sim[0];
+    s.pml_off = false;
     reset_sim(c, s, true);
     const int nt = c.grid.nt;
     const int n_shell = thickness > 0 ? static_cast<int>(c.shell_host.size()) : 0;
@@ -710,6 +739,11 @@ void forward_sim(Ctx& c, int thickness) {
         run_step(c, s, io, c.stream);
     }
     if (c.n_sens > 0) c.count(launch_check_finite(c.data, static_cast<long long>(nt) * c.n_sens, c.flags + 2, c.stream));
+}
+
+void forward_sim(Ctx& c, int thickness) {
+    forward_prep(c, thickness);
+    forward_steps(c, thickness);
 }
 
 // GradientAccumulator (gradient.hpp:50-142) for the selected parameter: which terms, their
@@ -735,18 +769,27 @@ void prepare_accumulator(Ctx& c) {
     } else {
         fail(USTFWI_ERR_INVALID, "unknown gradient parameter");
     }
+    if (!(pl.ddot == c.plan.ddot && pl.a1 == c.plan.a1 && pl.a2 == c.plan.a2 && pl.a1l == c.plan.a1l &&
+          pl.a2l == c.plan.a2l && pl.rho0 == c.plan.rho0))
+        c.touch();
     c.plan = pl;
     if (!pl.extra()) return;
     const size_t N = static_cast<size_t>(c.g.N);
     if (pl.rho0) {
         // rho0 as a coefficient (scalar when uniform) and 5 scratch fields in acc_mem
-        if (!c.acc_mem) c.acc_mem = c.alloc<float>(16 * N);
+        if (!c.acc_mem) {
+            c.acc_mem = c.alloc<float>(16 * N);
+            c.touch();
+        }
         bool uniform = true;
         for (size_t i = 1; i < N && uniform; ++i) uniform = c.rho0_host[i] == c.rho0_host[0];
         if (uniform) {
             c.rho0c = Coef{nullptr, static_cast<float>(c.rho0_host[0])};
         } else {
-            if (!c.rho0_field) c.rho0_field = c.alloc<float>(N);
+            if (!c.rho0_field) {
+                c.rho0_field = c.alloc<float>(N);
+                c.touch();
+            }
             const auto h = to_f32(c.rho0_host.data(), N);
             CK(cudaMemcpyAsync(c.rho0_field, h.data(), N * sizeof(float), cudaMemcpyHostToDevice, c.stream));
             CK(cudaStreamSynchronize(c.stream));
@@ -755,6 +798,7 @@ void prepare_accumulator(Ctx& c) {
         return;
     }
     if (!c.acc_mem) {
+        c.touch();
         c.acc_mem = c.alloc<float>(16 * N);
         for (int k = 0; k < 4; ++k) c.wa[k] = c.acc_mem + k * N;
         for (int r = 0; r < 3; ++r) {
@@ -894,22 +938,20 @@ void acc_correlate(Ctx& c, Correlate cr, int nw, int mid, int old, cudaStream_t 
 }
 
 // compute_gradient, TR branch (gradient.hpp:359-462), GradientParam c0 / alpha0 / y.
-void gradient_tr(Ctx& c, int thickness, bool accumulate, int slot = -1) {
-    require_medium(c);
-    if (c.gamma_host.empty()) fail(USTFWI_ERR_INVALID, "gradient computation requires a gamma mask");
-    if (!c.obs_ready) fail(USTFWI_ERR_INVALID, "observed data not uploaded");
-    if (thickness < 1) fail(USTFWI_ERR_INVALID, "shell thickness must be >= 1");
+// The device work of one TR gradient after the host-side preparation: forward with shell
+// record, adjoint source, interleaved adjoint + replay with the correlation into c.grad.
+// Only stream operations (kernel launches, memsets, events): captured as one CUDA graph.
+void gradient_core(Ctx& c, int thickness, bool accumulate) {
     const int nt = c.grid.nt, ns = c.n_sens, last = nt - 1;
-    forward_sim(c, thickness);
+    forward_steps(c, thickness);
     c.disp_active = c.dispersion && c.grad_dispersion;  // adjoint + replay steppers (gradient.hpp:381,424-426)
-    prepare_accumulator(c);
     // adjoint source: reverse, Kahan loss, integrate (gradient.hpp:264-289,378-379)
     c.count(launch_adjoint_source(c.data, c.obs, nt, ns, 1, c.q, c.loss_part, c.loss, c.loss + 1,
                                   accumulate ? 1 : 0, c.stream));
     c.launches += 1;  // loss reduction kernel
-    refresh_scales(c, c.adj);
     Sim& adj = c.sim[0];
     Sim& rep = c.sim[1];
+    rep.pml_off = false;
     reset_sim(c, adj, true);
     reset_sim(c, rep, false);
     CK(cudaMemsetAsync(c.grad, 0, static_cast<size_t>(c.g.N) * sizeof(float), c.stream));
@@ -985,6 +1027,62 @@ void gradient_tr(Ctx& c, int thickness, bool accumulate, int slot = -1) {
     if (dual) {
         CK(cudaEventRecord(c.ev_join, sb));
         CK(cudaStreamWaitEvent(sa, c.ev_join, 0));
+    }
+}
+
+bool use_graphs() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = std::getenv("USTFWI_GRAPH");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+// compute_gradient, TR branch (gradient.hpp:359-462). The device part (gradient_core, ~9
+// launches per simulation step = 105k launches at config D) is captured into a CUDA graph on
+// the second call with the same configuration (the first call runs eagerly and warms every
+// kernel's attributes) and replayed afterwards; any set_* call invalidates it (epoch).
+void gradient_tr(Ctx& c, int thickness, bool accumulate, int slot = -1) {
+    require_medium(c);
+    if (c.gamma_host.empty()) fail(USTFWI_ERR_INVALID, "gradient computation requires a gamma mask");
+    if (!c.obs_ready) fail(USTFWI_ERR_INVALID, "observed data not uploaded");
+    if (thickness < 1) fail(USTFWI_ERR_INVALID, "shell thickness must be >= 1");
+    forward_prep(c, thickness);
+    prepare_accumulator(c);
+    refresh_scales(c, c.adj);
+    const Ctx::GraphKey key{c.epoch, thickness, accumulate};
+    if (!use_graphs() || c.profiling) {
+        gradient_core(c, thickness, accumulate);
+    } else if (c.grad_graph && c.grad_key == key) {
+        CK(cudaGraphLaunch(c.grad_graph, c.stream));
+        c.launches += c.grad_graph_launches;
+    } else if (c.seen_key == key) {
+        c.drop_graph();
+        const uint64_t l0 = c.launches;
+        CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            gradient_core(c, thickness, accumulate);
+        } catch (...) {
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(c.stream, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamEndCapture(c.stream, &g));
+        const cudaError_t e = cudaGraphInstantiate(&c.grad_graph, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) {
+            c.grad_graph = nullptr;
+            fail(USTFWI_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+        }
+        c.grad_key = key;
+        c.grad_graph_launches = c.launches - l0;
+        CK(cudaGraphLaunch(c.grad_graph, c.stream));
+    } else {
+        gradient_core(c, thickness, accumulate);
+        c.seen_key = key;
     }
     if (slot >= 0) {
         // mini-batch slot: the masked gradient and this realization's loss
@@ -1232,6 +1330,7 @@ void ustfwi_gpu_destroy(ustfwi_gpu_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    c->drop_graph();
     if (c->comm) {
         try {
             nccl().comm_destroy(c->comm);
@@ -1257,6 +1356,7 @@ void ustfwi_gpu_destroy(ustfwi_gpu_ctx* c) {
 int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho0, const double* alpha0, double y,
                           const uint8_t* gamma, double c0_min, double c0_max) {
     return guarded(c, [&] {
+        c->touch();
         const size_t N = static_cast<size_t>(c->g.N);
         if (!c0 || !rho0) fail(USTFWI_ERR_INVALID, "medium fields must match the grid");
         // Medium::validate (medium.hpp:41-57); chunked over host threads, the first failing
@@ -1383,12 +1483,16 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
 }
 
 int ustfwi_gpu_set_gradient_options(ustfwi_gpu_ctx* c, int dispersion_enabled) {
-    return guarded(c, [&] { c->grad_dispersion = dispersion_enabled != 0; });
+    return guarded(c, [&] {
+        if (c->grad_dispersion != (dispersion_enabled != 0)) c->touch();
+        c->grad_dispersion = dispersion_enabled != 0;
+    });
 }
 
 int ustfwi_gpu_set_gradient_param(ustfwi_gpu_ctx* c, int param) {
     return guarded(c, [&] {
         if (param < 0 || param > 3) fail(USTFWI_ERR_INVALID, "unknown gradient parameter");
+        if (param != c->grad_param) c->touch();
         c->grad_param = param;
     });
 }
@@ -1396,6 +1500,7 @@ int ustfwi_gpu_set_gradient_param(ustfwi_gpu_ctx* c, int param) {
 int ustfwi_gpu_set_sources(ustfwi_gpu_ctx* c, size_t n_src, const size_t* pos, const size_t* sig_off,
                            const double* sig, const double* weights, const int32_t* delay_steps) {
     return guarded(c, [&] {
+        c->touch();
         const size_t N = static_cast<size_t>(c->g.N);
         std::vector<size_t> p(pos, pos + n_src);
         for (size_t v : p)
@@ -1786,6 +1891,7 @@ size_t ustfwi_gpu_shell_size(const ustfwi_gpu_ctx* c) { return c ? c->shell_host
 
 int ustfwi_gpu_set_profiling(ustfwi_gpu_ctx* c, int enable) {
     return guarded(c, [&] {
+        c->touch();
         CK(cudaStreamSynchronize(c->stream));
         c->resolve_profile();
         c->profiling = enable != 0;
