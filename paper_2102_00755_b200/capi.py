@@ -82,6 +82,18 @@ def lib():
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2102_00755_b200.build`"
                               " (there is no CPU fallback)")
+        if "USTFWI_NCCL_LIB" not in os.environ:
+            # the NCCL torch is built against (pip wheel), so that importing torch after the
+            # engine loaded NCCL does not bind torch to an older system libnccl
+            try:
+                import importlib.util
+                spec = importlib.util.find_spec("nvidia.nccl")
+                if spec and spec.submodule_search_locations:
+                    cand = os.path.join(list(spec.submodule_search_locations)[0], "lib", "libnccl.so.2")
+                    if os.path.exists(cand):
+                        os.environ["USTFWI_NCCL_LIB"] = cand
+            except Exception:
+                pass
         L = C.CDLL(LIB_PATH)
         L.ustfwi_last_error.restype = C.c_char_p
         L.ustfwi_version.restype = C.c_char_p

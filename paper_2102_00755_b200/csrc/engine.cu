@@ -98,7 +98,14 @@ struct NcclUniqueId {
 NcclApi& nccl() {
     static NcclApi api;
     if (!api.h) {
-        api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        // the NCCL a process already uses (e.g. torch's, loaded first) wins through the soname;
+        // otherwise USTFWI_NCCL_LIB (set by the Python layer to the pip NCCL that torch links,
+        // so that a later `import torch` finds the NCCL version it was built against), else
+        // the system libnccl.so.2
+        api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        const char* path = std::getenv("USTFWI_NCCL_LIB");
+        if (!api.h && path && *path) api.h = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
+        if (!api.h) api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (!api.h) fail(USTFWI_ERR_NCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
         api.get_unique_id = reinterpret_cast<int (*)(void*)>(dlsym(api.h, "ncclGetUniqueId"));
         api.all_gather = reinterpret_cast<int (*)(const void*, void*, size_t, int, void*, cudaStream_t)>(
