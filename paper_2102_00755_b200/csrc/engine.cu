@@ -4,6 +4,7 @@
 // and the device half of the C ABI (include/ustfwi_capi.h).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -22,6 +23,14 @@ using ustfwi_host::Error;
 using ustfwi_host::fail;
 
 namespace {
+
+// NVTX ranges (SURVEY §5.1 tracing): header-only nvtx3, a no-op unless a tool attaches
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 #define CK(expr)                                                                               \
     do {                                                                                       \
@@ -749,6 +758,7 @@ void forward_steps(Ctx& c, int thickness) {
 }
 
 void forward_sim(Ctx& c, int thickness) {
+    NvtxRange r("ustfwi forward");
     forward_prep(c, thickness);
     forward_steps(c, thickness);
 }
@@ -950,7 +960,11 @@ void acc_correlate(Ctx& c, Correlate cr, int nw, int mid, int old, cudaStream_t 
 // Only stream operations (kernel launches, memsets, events): captured as one CUDA graph.
 void gradient_core(Ctx& c, int thickness, bool accumulate) {
     const int nt = c.grid.nt, ns = c.n_sens, last = nt - 1;
-    forward_steps(c, thickness);
+    {
+        NvtxRange r("ustfwi forward (shell record)");
+        forward_steps(c, thickness);
+    }
+    NvtxRange r("ustfwi adjoint + time-reversal replay");
     c.disp_active = c.dispersion && c.grad_dispersion;  // adjoint + replay steppers (gradient.hpp:381,424-426)
     // adjoint source: reverse, Kahan loss, integrate (gradient.hpp:264-289,378-379)
     c.count(launch_adjoint_source(c.data, c.obs, nt, ns, 1, c.q, c.loss_part, c.loss, c.loss + 1,
@@ -1051,6 +1065,7 @@ bool use_graphs() {
 // the second call with the same configuration (the first call runs eagerly and warms every
 // kernel's attributes) and replayed afterwards; any set_* call invalidates it (epoch).
 void gradient_tr(Ctx& c, int thickness, bool accumulate, int slot = -1) {
+    NvtxRange range("ustfwi gradient_tr");
     require_medium(c);
     if (c.gamma_host.empty()) fail(USTFWI_ERR_INVALID, "gradient computation requires a gamma mask");
     if (!c.obs_ready) fail(USTFWI_ERR_INVALID, "observed data not uploaded");

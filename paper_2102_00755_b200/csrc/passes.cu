@@ -59,12 +59,10 @@ static __device__ __noinline__ float kpow_mult_call(float k2, float e, int kind)
 // ======================================================================================
 // Pencil passes (x and y)
 // ======================================================================================
-template <int L, int N1, int TB, bool DB, bool SPLIT = false>
+template <int L, int N1, int TB, bool DB>
 struct PencilCfg {
     static constexpr int N2 = L / N1;
-    // SPLIT: the N1 = 30 level runs as a thread pair (two 15-point prime-factor halves joined
-    // by a shuffle butterfly), so phase A has 2 * N2 * TB threads busy instead of N2 * TB
-    static constexpr int NT = SPLIT ? cmax(TB * N1, 2 * TB * N2) : TB * cmax(N1, N2);
+    static constexpr int NT = TB * cmax(N1, N2);
     static constexpr int KP = N2 * TB + 8;  // float2 pitch of one k1 slab (+64 B against bank conflicts)
     // Good-Thomas split when gcd(N1, N2) == 1: no inter-level twiddles
     static constexpr bool PFA = cx_gcd(N1, N2) == 1;
@@ -293,27 +291,11 @@ struct PencilMaps {
     CUtensorMap tm[3];  // per scratch buffer, the box shape of this pass
 };
 
-// 30-point DFT of a thread pair (lanes XOR_LANE apart) as the prime-factor split 2 x 15:
-// on entry thread h holds t_h[m] = v[(15 h + 2 m) mod 30], m < 15; on exit a[km] =
-// V[(15 h + 16 km) mod 30] (output map kr * 15 + km * 16, the CRT of 30 = 2 * 15).
-template <bool INV, int XOR_LANE>
-__device__ __forceinline__ void dft30_pair(float2 (&a)[15], int h) {
-    RDft<15, INV>::run(a);
-#pragma unroll
-    for (int km = 0; km < 15; ++km) {
-        float2 o;
-        o.x = __shfl_xor_sync(0xffffffffu, a[km].x, XOR_LANE);
-        o.y = __shfl_xor_sync(0xffffffffu, a[km].y, XOR_LANE);
-        a[km] = h ? csub(o, a[km]) : cadd(a[km], o);
-    }
-}
-
-template <int AXIS, bool INV, int L, int N1, int TB, int MINB, bool DB, bool SPLIT = false>
-__global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB, SPLIT>::NT, MINB)
+template <int AXIS, bool INV, int L, int N1, int TB, int MINB, bool DB>
+__global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
     pencil_tma_kernel(const __grid_constant__ GridDev g, const __grid_constant__ PencilJobs jobs,
                       const __grid_constant__ PencilMaps maps) {
-    using C = PencilCfg<L, N1, TB, DB, SPLIT>;
-    static_assert(!SPLIT || (N1 == 30 && !C::PFA), "the split phase A is the 30 = 2 x 15 level");
+    using C = PencilCfg<L, N1, TB, DB>;
     constexpr int N2 = C::N2, KP = C::KP, NT = C::NT;
     constexpr int NBUF = DB ? 2 : 1;
     constexpr int BOXR = L > 256 ? L / 2 : L;  // TMA box extent <= 256 rows
@@ -353,8 +335,6 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB, SPLIT>::NT, MINB)
     const int ra = threadIdx.x / TB;
     const bool inA = ra < N2, inB = ra < N1;
     const int kb = C::out_base(ra);
-    // split phase A: pair (n2, h) of 15-point halves, partner lane ^ TB
-    const int n2A = ra >> 1, hA = ra & 1;
     __syncthreads();  // barriers initialised, twiddles staged
 
     // tile coordinates of unit u: (float column, line, first row) in the 3-D tensor view
@@ -408,17 +388,7 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB, SPLIT>::NT, MINB)
 
         // forward transform of xs -> X (phase-B registers); xs is free afterwards
         auto forward = [&](float2 (&X)[N2]) {
-            if constexpr (SPLIT) {
-                float2 a[15];
-#pragma unroll
-                for (int m = 0; m < 15; ++m) a[m] = xs[C::in_row((15 * hA + 2 * m) % 30, n2A) * TB + c];
-                dft30_pair<false, TB>(a, hA);
-#pragma unroll
-                for (int km = 0; km < 15; ++km) {
-                    const int k1 = (15 * hA + 16 * km) % 30;
-                    ys[k1 * KP + n2A * TB + c] = (km == 0 && hA == 0) ? a[km] : cmul(a[km], tw[n2A * k1]);
-                }
-            } else if (inA) {
+            if (inA) {
                 float2 a[N1];
 #pragma unroll
                 for (int n1 = 0; n1 < N1; ++n1) a[n1] = xs[C::in_row(n1, ra) * TB + c];
@@ -453,14 +423,7 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB, SPLIT>::NT, MINB)
                 for (int n2 = 0; n2 < N2; ++n2) ys[ra * KP + n2 * TB + c] = bb[n2];
             }
             __syncthreads();
-            if constexpr (SPLIT) {
-                float2 a[15];
-#pragma unroll
-                for (int m = 0; m < 15; ++m) a[m] = ys[((15 * hA + 2 * m) % 30) * KP + n2A * TB + c];
-                dft30_pair<true, TB>(a, hA);
-#pragma unroll
-                for (int km = 0; km < 15; ++km) xs[C::in_row((15 * hA + 16 * km) % 30, n2A) * TB + c] = a[km];
-            } else if (inA) {
+            if (inA) {
                 float2 a[N1];
 #pragma unroll
                 for (int k1 = 0; k1 < N1; ++k1) a[k1] = ys[k1 * KP + ra * TB + c];
@@ -1492,15 +1455,15 @@ bool pencil_map(CUtensorMap* out, const float2* buf, const GridDev& g, int axis,
     return true;
 }
 
-template <int AXIS, bool INV, int L, int N1, int TB, int MINB, bool DB, bool SPLIT = false>
+template <int AXIS, bool INV, int L, int N1, int TB, int MINB, bool DB>
 cudaError_t run_pencil_tma(const GridDev& g, const PencilJobs& j, cudaStream_t st) {
-    using C = PencilCfg<L, N1, TB, DB, SPLIT>;
+    using C = PencilCfg<L, N1, TB, DB>;
     constexpr int BOXR = L > 256 ? L / 2 : L;
     PencilMaps maps;
     std::memset(&maps, 0, sizeof(maps));
     for (int f = 0; f < 3; ++f)
         if (j.buf[f] && !pencil_map(&maps.tm[f], j.buf[f], g, AXIS, TB, BOXR)) return cudaErrorInvalidValue;
-    auto kern = pencil_tma_kernel<AXIS, INV, L, N1, TB, MINB, DB, SPLIT>;
+    auto kern = pencil_tma_kernel<AXIS, INV, L, N1, TB, MINB, DB>;
     constexpr size_t smem = 128 + ((DB ? 2 : 1) * size_t(L) * TB + size_t(N1) * C::KP + L) * sizeof(float2) +
                             (AXIS == 0 ? size_t(L) * (TB + 1) * sizeof(float) : 0);
     static std::atomic<unsigned long long> configured{0};
@@ -1515,24 +1478,10 @@ cudaError_t run_pencil_tma(const GridDev& g, const PencilJobs& j, cudaStream_t s
 
 // x passes are instantiated in the main translation unit, y passes only in passes_y.cu
 // (compiled with USTFWI_FFT_SCALAR_ADD, fft_smem.cuh)
-// USTFWI_SPLITA bit 0: x pass, bit 1: y pass with the 30-point level split over thread pairs
-int split_mode() {
-    static const int v = [] {
-        const char* e = std::getenv("USTFWI_SPLITA");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
 template <int L, int N1, int TB, int MINB, bool DB>
 cudaError_t pencil_sized(int axis, bool inv, const GridDev& g, const PencilJobs& j, cudaStream_t st) {
 #ifdef USTFWI_PASSES_Y_ONLY
     if (axis != 1) return cudaErrorInvalidValue;
-    if constexpr (L == 480 && N1 == 30) {
-        if (use_pencil_tma() && (split_mode() & 2))
-            return inv ? run_pencil_tma<1, true, L, N1, TB, MINB, DB, true>(g, j, st)
-                       : run_pencil_tma<1, false, L, N1, TB, MINB, DB, true>(g, j, st);
-    }
     if (use_pencil_tma())
         return inv ? run_pencil_tma<1, true, L, N1, TB, MINB, DB>(g, j, st)
                    : run_pencil_tma<1, false, L, N1, TB, MINB, DB>(g, j, st);
@@ -1540,9 +1489,6 @@ cudaError_t pencil_sized(int axis, bool inv, const GridDev& g, const PencilJobs&
                : run_pencil<1, false, L, N1, TB, MINB, DB>(g, j, st);
 #else
     if (axis != 0) return cudaErrorInvalidValue;
-    if constexpr (L == 480 && N1 == 30) {
-        if (use_pencil_tma() && (split_mode() & 1)) return run_pencil_tma<0, false, L, N1, TB, MINB, DB, true>(g, j, st);
-    }
     if (use_pencil_tma()) return run_pencil_tma<0, false, L, N1, TB, MINB, DB>(g, j, st);
     return run_pencil<0, false, L, N1, TB, MINB, DB>(g, j, st);
 #endif

@@ -52,7 +52,6 @@ def run(env_extra, layout):
 @pytest.mark.parametrize("layout,variant", [
     ("y", {"USTFWI_PENCIL_TMA": "0"}), ("y", {"USTFWI_ZROW2": "0"}), ("y", {"USTFWI_GENERIC": "1"}),
     ("x", {"USTFWI_X480": "1"}), ("x", {"USTFWI_PENCIL_TMA": "0"}),
-    ("x", {"USTFWI_SPLITA": "1"}), ("y", {"USTFWI_SPLITA": "2"}),
 ])
 def test_kernel_variants_agree(layout, variant):
     base = run({}, layout)
