@@ -225,7 +225,8 @@ USTFWI_API size_t ustfwi_gpu_shell_size(const ustfwi_gpu_ctx* ctx);
 #define USTFWI_KERNEL_ZVEL 2 /* fused z c2r + velocity update + r2c */
 #define USTFWI_KERNEL_ZRHO 3 /* fused z c2r + density/pressure/sparse/correlation + r2c */
 #define USTFWI_KERNEL_AUX 4
-#define USTFWI_KERNEL_KINDS 5
+#define USTFWI_KERNEL_CHAIN 5 /* fused y-x-y chain (y forward, x * kappa * D_x * inverse, y inverse) */
+#define USTFWI_KERNEL_KINDS 6
 /* Enable/disable event timing of every launch and reset the counters. */
 USTFWI_API int ustfwi_gpu_set_profiling(ustfwi_gpu_ctx* ctx, int enable);
 /* Accumulated device time, launch count and algorithmic bytes (minimum HBM traffic of the

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(HERE, "libustfwi_b200.so")
 
 OK, ERR_INVALID, ERR_NUMERICAL, ERR_CUDA, ERR_OOM, ERR_NCCL = 0, 1, 2, 3, 4, 5
 STAGGER = {"none": 0, "plus": 1, "minus": 2}
-KERNEL_KINDS = ["y_pass", "x_pass", "z_vel", "z_rho", "aux"]
+KERNEL_KINDS = ["y_pass", "x_pass", "z_vel", "z_rho", "aux", "yxy_chain"]
 
 # Every symbol include/ustfwi_capi.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = [

@@ -41,7 +41,7 @@ struct NvtxRange {
     } while (0)
 
 enum { ST_NONE = 0, ST_PLUS = 1, ST_MINUS = 2, ST_SHIFT = 3, ST_SHIFTM = 4, ST_COUNT = 5 };
-enum { KIND_Y = 0, KIND_X = 1, KIND_ZVEL = 2, KIND_ZRHO = 3, KIND_AUX = 4 };
+enum { KIND_Y = 0, KIND_X = 1, KIND_ZVEL = 2, KIND_ZRHO = 3, KIND_AUX = 4, KIND_CHAIN = 5 };
 
 struct Sim {
     float* p = nullptr;
@@ -49,6 +49,7 @@ struct Sim {
     float* rho[3] = {};
     float2* S[3] = {};
     bool pml_off = false;   // StepperOptions::pml_enabled == false (engine.hpp:171,202-213)
+    int* chain_ctr = nullptr;  // claim / completion counters of this simulation's chain kernel
 };
 
 // WaveStepper options and counters of the step-level C ABI (engine.hpp:170-177,344-346)
@@ -449,84 +450,86 @@ void absorbing_tail(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     c.count(launch_abs_pressure(N, A, st));
     c.count(launch_gather(io.p_out, io.sens, st));
     c.count(launch_gather(io.p_out, io.shell, st));
-    c.count(launch_zfwd(c.g, io.p_out, s.S[0], st));
-    PencilJobs j{};
-    j.buf[0] = s.S[0];
-    j.n = 1;
-    j.job[0] = {0, 0, nullptr, 0, 0.f};
-    c.count(launch_pencil(1, false, c.g, j, st));
+    c.count(launch_zfwd(c.g, io.p_out, s.S[0], st));  // entry invariant of the next step: S0 = Fz p
+}
+
+// USTFWI_CHAIN=0 disables the fused y-x-y chain kernel (three pencil launches per chain)
+bool chain_enabled(const Ctx& c) {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = std::getenv("USTFWI_CHAIN");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1 && !use_generic_kernels() && use_pencil_tma() && chain_supported(c.g) && c.sim[0].chain_ctr;
 }
 
 // One leapfrog step of a stepper: update_velocity_density (engine.hpp:270-292), sparse
-// injection / shell enforcement, update_pressure (:318-347), gathers — 8 launches.
-// x-plane chunk of the y/z pass chains (0 = whole grid). With chunks, a chunk's
-// y-inverse -> z -> y-forward chain runs back to back so its spectra stay L2-resident.
-int chunk_planes(const Ctx& c) {
-    static int env = -1;
-    if (env < 0) {
-        const char* e = std::getenv("USTFWI_CHUNK");
-        env = e ? std::max(0, std::atoi(e)) : 0;
-    }
-    if (use_generic_kernels() || !fast_rows_supported(c.g.nz)) return 0;
-    return env;
-}
-
+// injection / shell enforcement, update_pressure (:318-347), gathers. Entry invariant: S0 holds
+// Fz p (the previous step's pressure kernel, or an initial state). The y / x / y passes on
+// either side of the velocity and density z passes form two "y-x-y chains":
+//   chain 1: Fy(S0); Fx -> kappa D_x+ / kappa -> Fx^-1; Fy^-1 (D_y+ on one output)
+//   chain 2: Fy(v_a spectra); Fx -> kappa D_x- / kappa -> Fx^-1; Fy^-1 (D_y- on v_y)
+// run either as three pencil launches each or as one persistent chain kernel that walks
+// kz-column slabs through the three passes with the slab's spectra resident in L2
+// (launch_chain, USTFWI_CHAIN).
 void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     const GridDev& g = c.g;
     const double SB = static_cast<double>(g.rows) * g.nzh * sizeof(float2);  // one half spectrum
     const double FB = static_cast<double>(g.N) * sizeof(float);               // one real field
-    const int ch = (chunk_planes(c) > 0 && !c.absorbing) ? std::min(chunk_planes(c), g.nx) : g.nx;
-    // run body(gc, frac) over the x-plane chunks
-    auto chunked = [&](auto&& body) {
-        for (int x0 = 0; x0 < g.nx; x0 += ch) {
-            GridDev gc = g;
-            gc.x0 = x0;
-            gc.xn = std::min(ch, g.nx - x0);
-            body(gc, static_cast<double>(gc.xn) / g.nx);
-        }
-    };
-    auto pencil = [&](const GridDev& gg, double frac, int axis, bool inv, const PencilJobs& j) {
+    auto pencil = [&](int axis, bool inv, const PencilJobs& j) {
         int loads = 0;
         for (int q = 0; q < j.n; ++q)
             if (q == 0 || j.job[q].src != j.job[q - 1].src) ++loads;
-        c.launch(axis == 0 ? KIND_X : KIND_Y, frac * (loads + j.n) * SB,
-                 [&] { return launch_pencil(axis, inv, gg, j, st); }, st);
+        c.launch(axis == 0 ? KIND_X : KIND_Y, (loads + j.n) * SB, [&] { return launch_pencil(axis, inv, g, j, st); }, st);
     };
-    PencilJobs j{};
-    for (int f = 0; f < 3; ++f) j.buf[f] = s.S[f];
-    // S0 holds Fy Fz p on entry (the previous step's pressure chain, or an initial state)
-    // X: (kappa D_x+ , kappa)
-    j.n = 2;
-    j.job[0] = {0, 0, c.dmul[0][ST_PLUS], 1};
-    j.job[1] = {0, 1, nullptr, 1};
-    pencil(g, 1.0, 0, false, j);
+    // one y-x-y chain: fused when supported, else three launches
+    auto chain = [&](const PencilJobs& ya, const PencilJobs& xb, const PencilJobs& yc) {
+        if (chain_enabled(c)) {
+            // algorithmic bytes of the fused chain: the first reads and the last writes only
+            int la = 0;
+            for (int q = 0; q < ya.n; ++q)
+                if (q == 0 || ya.job[q].src != ya.job[q - 1].src) ++la;
+            c.launch(KIND_CHAIN, (la + yc.n) * SB, [&] { return launch_chain(g, ya, xb, yc, s.chain_ctr, c.flags + 3, st); },
+                     st);
+        } else {
+            pencil(1, false, ya);
+            pencil(0, false, xb);
+            pencil(1, true, yc);
+        }
+    };
     float* const* stag = s.pml_off ? c.pml_one : c.pml_stag;
     float* const* regp = s.pml_off ? c.pml_one : c.pml_reg;
+    PencilJobs ya{}, xb{}, yc{};
+    for (int f = 0; f < 3; ++f) ya.buf[f] = xb.buf[f] = yc.buf[f] = s.S[f];
+    // chain 1: S0 <- Fy S0; X: S0 <- kappa D_x+ , S1 <- kappa; Y^-1: S0, S2 <- T_kappa, S1 <- D_y+ T_kappa
+    ya.n = 1;
+    ya.job[0] = {0, 0, nullptr, 0};
+    xb.n = 2;
+    xb.job[0] = {0, 0, c.dmul[0][ST_PLUS], 1};
+    xb.job[1] = {0, 1, nullptr, 1};
+    yc.n = 3;
+    yc.job[0] = {0, 0, nullptr, 0};
+    yc.job[1] = {1, 2, nullptr, 0};
+    yc.job[2] = {1, 1, c.dmul[1][ST_PLUS], 0};
+    chain(ya, xb, yc);
+    // Z: c2r (D_z+ on S2), velocity update, r2c of v
     Pml ps{{stag[0], stag[1], stag[2]}};
     const double coef_b = c.dtr_stag[0].field ? 3 * FB : 0.0;
-    chunked([&](const GridDev& gc, double frac) {
-        PencilJobs jj{};
-        for (int f = 0; f < 3; ++f) jj.buf[f] = s.S[f];
-        // Y inverse: S0 <- T_x, S2 <- T_kappa, S1 <- D_y+ T_kappa
-        jj.n = 3;
-        jj.job[0] = {0, 0, nullptr, 0};
-        jj.job[1] = {1, 2, nullptr, 0};
-        jj.job[2] = {1, 1, c.dmul[1][ST_PLUS], 0};
-        pencil(gc, frac, 1, true, jj);
-        // Z: c2r (D_z+ on S2), velocity update, r2c of v
-        c.launch(KIND_ZVEL, frac * (6 * SB + 6 * FB + coef_b),
-                 [&] { return launch_zvel(gc, s.S, c.dmul[2][ST_PLUS], s.v, ps, c.dtr_stag, st); }, st);
-        // Y forward x3
-        for (int f = 0; f < 3; ++f) jj.job[f] = {f, f, nullptr, 0};
-        pencil(gc, frac, 1, false, jj);
-    });
-    // X: kappa D_x-, kappa, kappa
-    j.n = 3;
-    j.job[0] = {0, 0, c.dmul[0][ST_MINUS], 1};
-    j.job[1] = {1, 1, nullptr, 1};
-    j.job[2] = {2, 2, nullptr, 1};
-    pencil(g, 1.0, 0, false, j);
-    // Z: c2r (D_z- on S2), density update, sparse ops, pressure, gathers, Fz p
+    c.launch(KIND_ZVEL, 6 * SB + 6 * FB + coef_b,
+             [&] { return launch_zvel(g, s.S, c.dmul[2][ST_PLUS], s.v, ps, c.dtr_stag, st); }, st);
+    // chain 2: Fy of Fz v_a; X: kappa D_x-, kappa, kappa; Y^-1 (D_y- on S1)
+    ya.n = 3;
+    for (int f = 0; f < 3; ++f) ya.job[f] = {f, f, nullptr, 0};
+    xb.n = 3;
+    xb.job[0] = {0, 0, c.dmul[0][ST_MINUS], 1};
+    xb.job[1] = {1, 1, nullptr, 1};
+    xb.job[2] = {2, 2, nullptr, 1};
+    yc.n = 3;
+    yc.job[0] = {0, 0, nullptr, 0};
+    yc.job[1] = {1, 1, c.dmul[1][ST_MINUS], 0};
+    yc.job[2] = {2, 2, nullptr, 0};
+    chain(ya, xb, yc);
+    // Z: c2r (D_z- on S2), density update, sparse ops, pressure, gathers, Fz p -> S0
     ZrhoArgs a{};
     for (int f = 0; f < 3; ++f) {
         a.S[f] = s.S[f];
@@ -562,34 +565,9 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     const bool split = !use_generic_kernels() && fast_rows_supported(g.nz);
     const double zb = 4 * SB + (split ? 11 : 8) * FB + (c.dtrho0.field ? FB : 0.0) + (io.corr.grad ? 5 * FB : 0.0);
     if (io.wait_before_z) CK(cudaStreamWaitEvent(st, io.wait_before_z, 0));
-    chunked([&](const GridDev& gc, double frac) {
-        PencilJobs jj{};
-        for (int f = 0; f < 3; ++f) jj.buf[f] = s.S[f];
-        // Y inverse x3 (D_y- on S1)
-        jj.n = 3;
-        jj.job[0] = {0, 0, nullptr, 0};
-        jj.job[1] = {1, 1, c.dmul[1][ST_MINUS], 0};
-        jj.job[2] = {2, 2, nullptr, 0};
-        pencil(gc, frac, 1, true, jj);
-        c.launch(KIND_ZRHO, frac * zb, [&] { return launch_zrho(gc, a, true, st); }, st);
-        if (split) ++c.launches;
-        if (c.absorbing || io.density_only) return;
-        // Y forward of Fz p for the next step
-        jj.n = 1;
-        jj.job[0] = {0, 0, nullptr, 0};
-        pencil(gc, frac, 1, false, jj);
-    });
+    c.launch(KIND_ZRHO, zb, [&] { return launch_zrho(g, a, true, st); }, st);
+    if (split) ++c.launches;
     if (c.absorbing && !io.density_only) absorbing_tail(c, s, io, st);
-}
-
-// Y forward of S0 (after a pressure refresh outside run_step): restores the run_step
-// entry invariant S0 = Fy Fz p.
-void y_forward_p(Ctx& c, Sim& s, cudaStream_t st) {
-    PencilJobs j{};
-    j.buf[0] = s.S[0];
-    j.n = 1;
-    j.job[0] = {0, 0, nullptr, 0};
-    c.count(launch_pencil(1, false, c.g, j, st));
 }
 
 // blk8[b] = index of the first sorted position >= b * 8 rows (b = 0 .. ceil(rows/8)): the
@@ -711,15 +689,16 @@ void prepare_shell(Ctx& c, int thickness) {
 }
 
 void clear_flags(Ctx& c) {
-    const int init[3] = {INT_MAX, 0, 0};
+    const int init[4] = {INT_MAX, 0, 0, 0};
     CK(cudaMemcpyAsync(c.flags, init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
 }
 
 void check_flags(Ctx& c, bool grad_phase) {
-    int f[3];
+    int f[4];
     CK(cudaMemcpyAsync(f, c.flags, sizeof(f), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
     c.resolve_profile();
+    if (f[3]) fail(USTFWI_ERR_CUDA, "y-x-y chain kernel: a dependency wait timed out");
     if (f[0] != INT_MAX) fail(USTFWI_ERR_NUMERICAL, "pressure field diverged at step " + std::to_string(f[0]));
     if (f[2]) fail(USTFWI_ERR_NUMERICAL, "sensor data contains non-finite values");
     if (grad_phase && f[1]) fail(USTFWI_ERR_NUMERICAL, "gradient contains non-finite values");
@@ -1007,7 +986,6 @@ void gradient_core(Ctx& c, int thickness, bool accumulate) {
         a.enf = SparseEnforce{n_shell, c.shell_pos, shell_row(last), static_cast<float>(c.ndim), c.shell_blk8};
         a.diverged = c.flags;
         c.count(launch_zrho(c.g, a, false, sb));
-        y_forward_p(c, rep, sb);
         acc_push(c, rep, 0, sb);  // GradientAccumulator::push of the initial value (gradient.hpp:147-160)
     }
     // look-ahead step (gradient.hpp:438-441)
@@ -1319,7 +1297,9 @@ int ustfwi_gpu_create(int device, const ustfwi_grid* grid, ustfwi_gpu_ctx** out)
         // state of two steppers, the replay ring, gradient and accumulator
         const size_t N = static_cast<size_t>(g.N);
         const size_t NS = static_cast<size_t>(g.rows) * g.nzp;
+        const int ntx8 = (g.nzh + 7) / 8;
         for (int s = 0; s < 2; ++s) {
+            c->sim[s].chain_ctr = c->alloc<int>(static_cast<size_t>(1 + 3 * ntx8));
             for (int a = 0; a < 3; ++a) {
                 c->sim[s].v[a] = c->alloc<float>(N);
                 c->sim[s].rho[a] = c->alloc<float>(N);
@@ -1701,7 +1681,7 @@ void stage_sparse(Ctx& c, size_t n, const size_t* idx, const std::vector<float>&
     CK(cudaMemcpyAsync(c.stp_idx, ii.data(), n * sizeof(int), cudaMemcpyHostToDevice, c.stream));
     CK(cudaMemcpyAsync(c.stp_val, val.data(), n * sizeof(float), cudaMemcpyHostToDevice, c.stream));
 }
-// p = c0^2 sum_a rho_a and the entry invariant S0 = Fy Fz p of the next step
+// p = c0^2 sum_a rho_a and the entry invariant S0 = Fz p of the next step
 void stepper_pressure(Ctx& c, Sim& s, int check_step) {
     ZrhoArgs a{};
     for (int f = 0; f < 3; ++f) {
@@ -1716,7 +1696,6 @@ void stepper_pressure(Ctx& c, Sim& s, int check_step) {
     a.check_step = check_step;
     a.diverged = c.flags;
     c.count(launch_zrho(c.g, a, false, c.stream));
-    y_forward_p(c, s, c.stream);
 }
 }  // namespace
 

@@ -1494,6 +1494,361 @@ cudaError_t pencil_sized(int axis, bool inv, const GridDev& g, const PencilJobs&
 #endif
 }
 
+#ifndef USTFWI_PASSES_Y_ONLY
+// ======================================================================================
+// y-x-y chain: one persistent launch for Fy -> (Fx, multiply, Fx^-1) -> Fy^-1
+// ======================================================================================
+// The two pencil chains of a step (run_step) each read and write every spectrum three times
+// when run as separate launches (18 S per voxel for the density chain). Here the grid is cut
+// into kz-column slabs (TB columns, all x and y: 480 x 480 x 8 complex = 14.7 MB per field at
+// config D) and the units of a slab run in order: phase A = y-forward tiles (one per x plane),
+// phase B = x tiles (one per y line, kappa / D_x and the inverse x FFT), phase C = y-inverse
+// tiles. A slab's spectra are written and re-read within tens of microseconds, so phases B
+// and C hit L2 and each spectrum crosses HBM once each way (6 S instead of 18 S).
+//
+// Scheduling: units are claimed in global order (slab-major, phases in order) by an atomic
+// counter; a unit's dependencies (all A units of its slab for B, all B units for C) are units
+// claimed earlier. A CTA computes its units in claim order, prefetches the next unit's tile
+// only when that unit's dependencies are already met, and before it blocks on a dependency
+// it has signalled every unit it computed, so the smallest waiting unit always has all its
+// producers running or done: no deadlock, and no CTA co-residency is assumed. Completion is
+// signalled lazily (one unit later, `cp.async.bulk.wait_group N`) after the TMA stores have
+// landed: async-proxy writes -> fence.proxy.async -> release atomic; consumers acquire the
+// counter and fence before their TMA loads. Waits are bounded: after ~2^24 polls the kernel
+// raises an error flag (checked on the host) instead of hanging.
+struct ChainArgs {
+    PencilJobs ph[3];   // phase A (y forward), B (x), C (y inverse)
+    PencilMaps mx, my;  // tensor maps of the scratch buffers: x-pencil boxes, y-pencil boxes
+    int* ctr;           // [0] claim counter, [1 + 3 s + p] completed units of slab s, phase p
+    int* err;           // set on a dependency-wait timeout
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_n() { asm volatile("cp.async.bulk.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int L, int N1, int TB, int MINB>
+__global__ void __launch_bounds__(PencilCfg<L, N1, TB, true>::NT, MINB)
+    chain_kernel(const __grid_constant__ GridDev g, const __grid_constant__ ChainArgs A) {
+    using C = PencilCfg<L, N1, TB, true>;
+    constexpr int N2 = C::N2, KP = C::KP, NT = C::NT;
+    constexpr int BOXR = L > 256 ? L / 2 : L;  // TMA box extent <= 256 rows
+    constexpr int NBOX = L / BOXR;
+    constexpr unsigned TILE_BYTES = unsigned(L) * TB * sizeof(float2);
+    extern __shared__ __align__(128) unsigned char sm_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm_raw);   // one per stage
+    int* s_unit = reinterpret_cast<int*>(sm_raw + 64);     // unit of each stage
+    int* s_loaded = s_unit + 2;                             // tile load issued for the stage
+    float2* xbuf = reinterpret_cast<float2*>(sm_raw + 128);  // [2][L][TB]
+    float2* ys = xbuf + 2 * L * TB;
+    float2* tw = ys + N1 * KP;
+    float* kap_s = reinterpret_cast<float*>(tw + L);
+    float* hkx2_s = kap_s + L * TB;
+    const bool producer = threadIdx.x == NT - 1;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+    }
+    for (int i = threadIdx.x; i < L; i += NT) {
+        tw[i] = g.px.tw[i];
+        const float hk = g.half_cdt * g.kx[i];
+        hkx2_s[i] = hk * hk;
+    }
+    // source groups of the three phases' job lists
+    int gs[3][5], ng[3];
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+        ng[p] = 0;
+        for (int jb = 0; jb < A.ph[p].n; ++jb)
+            if (jb == 0 || A.ph[p].job[jb].src != A.ph[p].job[jb - 1].src) gs[p][ng[p]++] = jb;
+        gs[p][ng[p]] = A.ph[p].n;
+    }
+    const int ntx = (g.nzh + TB - 1) / TB;
+    const int per_slab = 2 * g.nx + g.ny;
+    const int total = per_slab * ntx;
+    const int c = threadIdx.x % TB;
+    const int ra = threadIdx.x / TB;
+    const bool inA = ra < N2, inB = ra < N1;
+    const int kb = C::out_base(ra);
+
+    auto decode = [&](int u, int& slab, int& phase, int& line) {
+        slab = u / per_slab;
+        const int r = u - slab * per_slab;
+        if (r < g.nx) {
+            phase = 0;
+            line = r;
+        } else if (r < g.nx + g.ny) {
+            phase = 1;
+            line = r - g.nx;
+        } else {
+            phase = 2;
+            line = r - g.nx - g.ny;
+        }
+    };
+    auto ready = [&](int u) {
+        int slab, phase, line;
+        decode(u, slab, phase, line);
+        if (phase == 0) return true;
+        return ld_acquire(A.ctr + 1 + 3 * slab + phase - 1) >= (phase == 1 ? g.nx : g.ny);
+    };
+    auto box = [&](int phase, int buf, float2* s, int line, int col0, int q, bool load, uint64_t* b) {
+        const int r0 = q * BOXR;
+        const int e0 = 2 * col0;
+        const CUtensorMap* tm = phase == 1 ? &A.mx.tm[buf] : &A.my.tm[buf];
+        const int e1 = phase == 1 ? line : r0;
+        const int e2 = phase == 1 ? r0 : line;
+        if (load) tma_load_3d(s + r0 * TB, tm, e0, e1, e2, b);
+        else tma_store_3d(tm, s + r0 * TB, e0, e1, e2);
+    };
+    auto load_unit = [&](int u, int b) {  // producer only
+        int slab, phase, line;
+        decode(u, slab, phase, line);
+        float2* xs = xbuf + b * L * TB;
+        bulk_wait_read_all();  // the stage may still be the source of a store
+        fence_proxy_async_global();
+        mbar_arrive_expect_tx(&bar[b], TILE_BYTES);
+        const int src = A.ph[phase].job[0].src;
+#pragma unroll
+        for (int q = 0; q < NBOX; ++q) box(phase, src, xs, line, slab * TB, q, true, &bar[b]);
+    };
+    // producer-side lazy completion: the last computed unit and its store-group count
+    int prev_slot = -1, prev_groups = 0;
+    auto signal_prev_all = [&]() {  // producer only: every computed unit complete and counted
+        if (prev_slot >= 0) {
+            bulk_wait_all();
+            fence_proxy_async_global();
+            __threadfence();
+            atomicAdd(A.ctr + prev_slot, 1);
+            prev_slot = -1;
+        }
+    };
+    auto wait_ready = [&](int u) {  // producer only, blocking (bounded)
+        unsigned spins = 0;
+        while (!ready(u)) {
+            __nanosleep(64);
+            if (++spins > (1u << 24)) {
+                atomicExch(A.err, 1);
+                break;
+            }
+        }
+    };
+
+    if (producer) {
+        const int u0 = atomicAdd(A.ctr, 1);
+        s_unit[0] = u0;
+        s_loaded[0] = 0;
+        if (u0 < total && ready(u0)) {
+            load_unit(u0, 0);
+            s_loaded[0] = 1;
+        }
+    }
+    unsigned uses[2] = {0u, 0u};
+    int b = 0;
+    for (;;) {
+        __syncthreads();  // s_unit / s_loaded of stage b visible; previous unit's smem reads done
+        const int u = s_unit[b];
+        if (u >= total) break;
+        if (producer) {
+            if (!s_loaded[b]) {
+                signal_prev_all();
+                wait_ready(u);
+                load_unit(u, b);
+            }
+            const int nu = atomicAdd(A.ctr, 1);
+            s_unit[b ^ 1] = nu;
+            s_loaded[b ^ 1] = 0;
+            if (nu < total && ready(nu)) {
+                load_unit(nu, b ^ 1);
+                s_loaded[b ^ 1] = 1;
+            }
+        }
+        mbar_wait(&bar[b], uses[b] & 1);
+        ++uses[b];
+        int slab, phase, line;
+        decode(u, slab, phase, line);
+        const int col0 = slab * TB;
+        const PencilJobs& jobs = A.ph[phase];
+        float2* xs = xbuf + b * L * TB;
+        int groups = 0;
+
+        auto store_tile = [&](int dst) {
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (producer) {
+#pragma unroll
+                for (int q = 0; q < NBOX; ++q) box(phase, dst, xs, line, col0, q, false, nullptr);
+                bulk_commit();
+            }
+            ++groups;
+        };
+        auto forward = [&](float2 (&X)[N2]) {
+            if (inA) {
+                float2 a[N1];
+#pragma unroll
+                for (int n1 = 0; n1 < N1; ++n1) a[n1] = xs[C::in_row(n1, ra) * TB + c];
+                RDft<N1, false>::run(a);
+                if constexpr (!C::PFA) {
+#pragma unroll
+                    for (int k1 = 1; k1 < N1; ++k1) a[k1] = cmul(a[k1], tw[ra * k1]);
+                }
+#pragma unroll
+                for (int k1 = 0; k1 < N1; ++k1) ys[k1 * KP + ra * TB + c] = a[k1];
+            }
+            __syncthreads();
+            if (inB) {
+#pragma unroll
+                for (int n2 = 0; n2 < N2; ++n2) X[n2] = ys[ra * KP + n2 * TB + c];
+                RDft<N2, false>::run(X);
+            }
+        };
+        auto inverse_store = [&](float2 (&bb)[N2], int dst) {
+            if (inB) {
+                RDft<N2, true>::run(bb);
+                if constexpr (!C::PFA) {
+#pragma unroll
+                    for (int n2 = 1; n2 < N2; ++n2) bb[n2] = cmul(bb[n2], conjf2(tw[ra * n2]));
+                }
+            }
+            if (producer) bulk_wait_read_all();  // previous store out of xs
+            __syncthreads();
+            if (inB) {
+#pragma unroll
+                for (int n2 = 0; n2 < N2; ++n2) ys[ra * KP + n2 * TB + c] = bb[n2];
+            }
+            __syncthreads();
+            if (inA) {
+                float2 a[N1];
+#pragma unroll
+                for (int k1 = 0; k1 < N1; ++k1) a[k1] = ys[k1 * KP + ra * TB + c];
+                RDft<N1, true>::run(a);
+#pragma unroll
+                for (int n1 = 0; n1 < N1; ++n1) xs[C::in_row(n1, ra) * TB + c] = a[n1];
+            }
+            store_tile(dst);
+        };
+
+        float2 X[N2];
+        if (phase == 0) {
+            // y forward, every job of the phase is an in-place transform of its own source
+            for (int gi = 0; gi < ng[0]; ++gi) {
+                if (gi > 0) {
+                    // further sources of phase A (the 3-field chain): load synchronously
+                    __syncthreads();
+                    if (producer) {
+                        bulk_wait_read_all();
+                        mbar_arrive_expect_tx(&bar[b], TILE_BYTES);
+#pragma unroll
+                        for (int q = 0; q < NBOX; ++q) box(0, jobs.job[gs[0][gi]].src, xs, line, col0, q, true, &bar[b]);
+                    }
+                    mbar_wait(&bar[b], uses[b] & 1);
+                    ++uses[b];
+                }
+                forward(X);
+                if (inB) {
+#pragma unroll
+                    for (int k2 = 0; k2 < N2; ++k2) xs[C::out_row(kb, k2) * TB + c] = X[k2];
+                }
+                store_tile(jobs.job[gs[0][gi]].dst);
+            }
+        } else {
+            for (int grp = 0; grp < ng[phase]; ++grp) {
+                const int gb = gs[phase][grp], ge = gs[phase][grp + 1];
+                if (grp > 0) {
+                    __syncthreads();
+                    if (producer) {
+                        bulk_wait_read_all();
+                        mbar_arrive_expect_tx(&bar[b], TILE_BYTES);
+#pragma unroll
+                        for (int q = 0; q < NBOX; ++q) box(phase, jobs.job[gb].src, xs, line, col0, q, true, &bar[b]);
+                    }
+                    mbar_wait(&bar[b], uses[b] & 1);
+                    ++uses[b];
+                }
+                if (phase == 1) {
+                    forward(X);
+                    if (inB && jobs.job[gb].kappa) {
+                        if (grp == 0) {
+                            const float ky = g.ky[line];
+                            const float kz = col0 + c < g.nzh ? g.kz[col0 + c] : 0.f;
+                            const float hy = g.half_cdt * ky, hz = g.half_cdt * kz;
+                            const float uyz = hy * hy + hz * hz;
+#pragma unroll
+                            for (int k2 = 0; k2 < N2; ++k2) {
+                                const int k = C::out_row(kb, k2);
+                                kap_s[k * TB + c] = kappa_of_u(hkx2_s[k] + uyz);
+                            }
+                        }
+#pragma unroll
+                        for (int k2 = 0; k2 < N2; ++k2) X[k2] = cscale(X[k2], kap_s[C::out_row(kb, k2) * TB + c]);
+                    }
+                } else if (inB) {
+#pragma unroll
+                    for (int k2 = 0; k2 < N2; ++k2) X[k2] = xs[C::out_row(kb, k2) * TB + c];
+                }
+                for (int jb = gb; jb < ge; ++jb) {
+                    const PencilJob J = jobs.job[jb];
+                    float2 bb[N2];
+                    if (inB) {
+#pragma unroll
+                        for (int k2 = 0; k2 < N2; ++k2)
+                            bb[k2] = J.dmul ? cmul(X[k2], __ldg(J.dmul + C::out_row(kb, k2))) : X[k2];
+                    }
+                    inverse_store(bb, J.dst);
+                }
+            }
+        }
+        if (producer) {
+            // lazy completion: the previous unit's stores are older than this unit's groups
+            if (prev_slot >= 0) {
+                if (groups >= 3) bulk_wait_n<3>();
+                else if (groups == 2) bulk_wait_n<2>();
+                else bulk_wait_n<1>();
+                fence_proxy_async_global();
+                __threadfence();
+                atomicAdd(A.ctr + prev_slot, 1);
+            }
+            prev_slot = 1 + 3 * slab + phase;
+        }
+        b ^= 1;
+    }
+    if (producer) signal_prev_all();
+}
+
+template <int L, int N1, int TB, int MINB>
+cudaError_t run_chain(const GridDev& g, const PencilJobs& ya, const PencilJobs& xb, const PencilJobs& yc, int* ctr,
+                      int* err, cudaStream_t st) {
+    using C = PencilCfg<L, N1, TB, true>;
+    constexpr int BOXR = L > 256 ? L / 2 : L;
+    ChainArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.ph[0] = ya;
+    a.ph[1] = xb;
+    a.ph[2] = yc;
+    for (int f = 0; f < 3; ++f)
+        if (ya.buf[f]) {
+            if (!pencil_map(&a.mx.tm[f], ya.buf[f], g, 0, TB, BOXR)) return cudaErrorInvalidValue;
+            if (!pencil_map(&a.my.tm[f], ya.buf[f], g, 1, TB, BOXR)) return cudaErrorInvalidValue;
+        }
+    a.ctr = ctr;
+    a.err = err;
+    const int ntx = (g.nzh + TB - 1) / TB;
+    cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(int) * (1 + 3 * ntx), st);
+    if (e != cudaSuccess) return e;
+    auto kern = chain_kernel<L, N1, TB, MINB>;
+    constexpr size_t smem = 128 + (2 * size_t(L) * TB + size_t(N1) * C::KP + L) * sizeof(float2) +
+                            size_t(L) * (TB + 1) * sizeof(float);
+    static std::atomic<unsigned long long> configured{0};
+    once_per_device(configured, [&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
+    kern<<<sm_count() * MINB, C::NT, smem, st>>>(g, a);
+    return cudaGetLastError();
+}
+#endif  // !USTFWI_PASSES_Y_ONLY
+
 }  // namespace
 
 #ifdef USTFWI_PASSES_Y_ONLY
@@ -1545,6 +1900,16 @@ cudaError_t launch_pencil_fast(int axis, bool inv, const GridDev& g, const Penci
             return cudaErrorInvalidValue;
         default: return cudaErrorInvalidValue;
     }
+}
+
+// the fused y-x-y chain is compiled for the 480-point lines of config D / E level 2 (x and y
+// share the plan) and 2 CTAs per SM
+bool chain_supported(const GridDev& g) { return g.nx == 480 && g.ny == 480 && g.x0 == 0 && g.xn == g.nx; }
+
+cudaError_t launch_chain(const GridDev& g, const PencilJobs& ya, const PencilJobs& xb, const PencilJobs& yc, int* ctr,
+                         int* err, cudaStream_t st) {
+    if (!chain_supported(g)) return cudaErrorInvalidValue;
+    return run_chain<480, 30, 8, 2>(g, ya, xb, yc, ctr, err, st);
 }
 
 bool fast_rows_supported(int nz) {

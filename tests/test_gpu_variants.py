@@ -2,7 +2,8 @@
 z kernels, USTFWI_GENERIC=1: runtime-plan Stockham kernels, USTFWI_X480=1: 32x15 x pass)
 compute the same step: forward traces of a grid that selects the 480-point y pencils and
 the nz = 256 z kernels agree across variants (each variant in its own process, the switches
-are read once)."""
+are read once). On a 480 x 480 x 32 grid the fused y-x-y chain kernel (default) and the three
+separate pencil launches (USTFWI_CHAIN=0) give the same traces and TR gradient."""
 import json
 import os
 import subprocess
@@ -20,7 +21,7 @@ import numpy as np
 sys.path.insert(0, sys.argv[1])
 from paper_2102_00755_b200 import capi
 from paper_2102_00755_b200.engine import GpuEngine, Medium, SensorArray, SourceSet
-dims = [480, 16, 256] if sys.argv[2] == "x" else [8, 480, 256]
+dims = {"x": [480, 16, 256], "y": [8, 480, 256], "xy": [480, 480, 32]}[sys.argv[2]]
 g = capi.grid_from(dims, 1e-3, 0.3e-3 / 1800.0, 40, [0, 0, 0], 1800.0)
 sh = g.shape
 f = lambda x, y, z: (x * sh[1] + y) * sh[2] + z
@@ -36,7 +37,13 @@ with GpuEngine(g) as eng:
     eng.set_sources(src)
     eng.set_sensors(sens)
     data, _ = eng.forward(0)
-print(json.dumps(data.tolist()))
+    if sys.argv[2] == "xy":  # a TR gradient too (both y-x-y chains, two streams, graph replay)
+        m.gamma = capi.ball_mask(sh, c, 6.0)
+        eng.set_medium(m)
+        for _ in range(3):
+            loss, grad = eng.gradient_tr(np.zeros_like(data), 2)
+        data = np.concatenate([data.ravel(), grad.ravel()[::97], [loss]])
+print(json.dumps(np.asarray(data).tolist()))
 '''
 
 
@@ -52,6 +59,7 @@ def run(env_extra, layout):
 @pytest.mark.parametrize("layout,variant", [
     ("y", {"USTFWI_PENCIL_TMA": "0"}), ("y", {"USTFWI_ZROW2": "0"}), ("y", {"USTFWI_GENERIC": "1"}),
     ("x", {"USTFWI_X480": "1"}), ("x", {"USTFWI_PENCIL_TMA": "0"}),
+    ("xy", {"USTFWI_CHAIN": "0"}), ("xy", {"USTFWI_GRAPH": "0"}),
 ])
 def test_kernel_variants_agree(layout, variant):
     base = run({}, layout)
