@@ -45,7 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(err)
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", *objs, "-o", tmp, "-ldl"]
+    # --no-undefined: a missing symbol fails the build, not the first dlopen on the GPU box
+    cmd = [NVCC, *ARCH, "-shared", *objs, "-o", tmp, "-ldl", "-lpthread", "-lrt", "-Xlinker", "--no-undefined"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

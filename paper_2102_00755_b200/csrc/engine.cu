@@ -460,7 +460,7 @@ bool chain_enabled(const Ctx& c) {
         const char* e = std::getenv("USTFWI_CHAIN");
         on = (e && e[0] == '0') ? 0 : 1;
     }
-    return on == 1 && !use_generic_kernels() && use_pencil_tma() && chain_supported(c.g) && c.sim[0].chain_ctr;
+    return on == 1 && !use_generic_kernels() && chain_supported(c.g) && c.sim[0].chain_ctr;
 }
 
 // One leapfrog step of a stepper: update_velocity_density (engine.hpp:270-292), sparse

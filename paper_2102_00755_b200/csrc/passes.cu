@@ -1904,7 +1904,9 @@ cudaError_t launch_pencil_fast(int axis, bool inv, const GridDev& g, const Penci
 
 // the fused y-x-y chain is compiled for the 480-point lines of config D / E level 2 (x and y
 // share the plan) and 2 CTAs per SM
-bool chain_supported(const GridDev& g) { return g.nx == 480 && g.ny == 480 && g.x0 == 0 && g.xn == g.nx; }
+bool chain_supported(const GridDev& g) {
+    return g.nx == 480 && g.ny == 480 && g.x0 == 0 && g.xn == g.nx && use_pencil_tma();
+}
 
 cudaError_t launch_chain(const GridDev& g, const PencilJobs& ya, const PencilJobs& xb, const PencilJobs& yc, int* ctr,
                          int* err, cudaStream_t st) {
