@@ -1521,6 +1521,8 @@ struct ChainArgs {
     PencilMaps mx, my;  // tensor maps of the scratch buffers: x-pencil boxes, y-pencil boxes
     int* ctr;           // [0] claim counter, [1 + 3 s + p] completed units of slab s, phase p
     int* err;           // set on a dependency-wait timeout
+    int nbatch;         // claim order: batch q = (phase, slab) of `lines` consecutive units
+    unsigned char bphase[64], bslab[64];
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -1532,6 +1534,12 @@ __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence
 template <int N>
 __device__ __forceinline__ void bulk_wait_n() { asm volatile("cp.async.bulk.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// Units are tiles of one (phase, slab) batch; a CTA walks "tile steps" (unit, source group)
+// through two TMA stages: while one tile is transformed the next one (the next source group of
+// the same unit, or the first tile of the next claimed unit when its dependencies are met)
+// is in flight. Batches are claimed in the order A0 A1 B0 B1 C0, then (A k, C k-1, B k) for
+// k >= 2, then the last C: every batch's producers were claimed at least one batch earlier
+// (no phase-boundary drain) while at most two slabs are live in L2.
 template <int L, int N1, int TB, int MINB>
 __global__ void __launch_bounds__(PencilCfg<L, N1, TB, true>::NT, MINB)
     chain_kernel(const __grid_constant__ GridDev g, const __grid_constant__ ChainArgs A) {
@@ -1542,8 +1550,9 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, true>::NT, MINB)
     constexpr unsigned TILE_BYTES = unsigned(L) * TB * sizeof(float2);
     extern __shared__ __align__(128) unsigned char sm_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm_raw);   // one per stage
-    int* s_unit = reinterpret_cast<int*>(sm_raw + 64);     // unit of each stage
-    int* s_loaded = s_unit + 2;                             // tile load issued for the stage
+    int* s_unit = reinterpret_cast<int*>(sm_raw + 64);     // [2] unit of each stage
+    int* s_grp = s_unit + 2;                                // [2] source group of each stage
+    int* s_loaded = s_unit + 4;                             // [2] tile load issued
     float2* xbuf = reinterpret_cast<float2*>(sm_raw + 128);  // [2][L][TB]
     float2* ys = xbuf + 2 * L * TB;
     float2* tw = ys + N1 * KP;
@@ -1568,33 +1577,24 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, true>::NT, MINB)
             if (jb == 0 || A.ph[p].job[jb].src != A.ph[p].job[jb - 1].src) gs[p][ng[p]++] = jb;
         gs[p][ng[p]] = A.ph[p].n;
     }
-    const int ntx = (g.nzh + TB - 1) / TB;
-    const int per_slab = 2 * g.nx + g.ny;
-    const int total = per_slab * ntx;
+    const int lines = g.nx;  // == g.ny (chain_supported)
+    const int total = lines * A.nbatch;
     const int c = threadIdx.x % TB;
     const int ra = threadIdx.x / TB;
     const bool inA = ra < N2, inB = ra < N1;
     const int kb = C::out_base(ra);
 
     auto decode = [&](int u, int& slab, int& phase, int& line) {
-        slab = u / per_slab;
-        const int r = u - slab * per_slab;
-        if (r < g.nx) {
-            phase = 0;
-            line = r;
-        } else if (r < g.nx + g.ny) {
-            phase = 1;
-            line = r - g.nx;
-        } else {
-            phase = 2;
-            line = r - g.nx - g.ny;
-        }
+        const int q = u / lines;
+        line = u - q * lines;
+        phase = A.bphase[q];
+        slab = A.bslab[q];
     };
     auto ready = [&](int u) {
         int slab, phase, line;
         decode(u, slab, phase, line);
         if (phase == 0) return true;
-        return ld_acquire(A.ctr + 1 + 3 * slab + phase - 1) >= (phase == 1 ? g.nx : g.ny);
+        return ld_acquire(A.ctr + 1 + 3 * slab + phase - 1) >= lines;
     };
     auto box = [&](int phase, int buf, float2* s, int line, int col0, int q, bool load, uint64_t* b) {
         const int r0 = q * BOXR;
@@ -1605,19 +1605,19 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, true>::NT, MINB)
         if (load) tma_load_3d(s + r0 * TB, tm, e0, e1, e2, b);
         else tma_store_3d(tm, s + r0 * TB, e0, e1, e2);
     };
-    auto load_unit = [&](int u, int b) {  // producer only
+    auto load_tile = [&](int u, int gi, int b) {  // producer only
         int slab, phase, line;
         decode(u, slab, phase, line);
         float2* xs = xbuf + b * L * TB;
         bulk_wait_read_all();  // the stage may still be the source of a store
         fence_proxy_async_global();
         mbar_arrive_expect_tx(&bar[b], TILE_BYTES);
-        const int src = A.ph[phase].job[0].src;
+        const int src = A.ph[phase].job[gs[phase][gi]].src;
 #pragma unroll
         for (int q = 0; q < NBOX; ++q) box(phase, src, xs, line, slab * TB, q, true, &bar[b]);
     };
-    // producer-side lazy completion: the last computed unit and its store-group count
-    int prev_slot = -1, prev_groups = 0;
+    // producer-side lazy completion: the last computed unit (counter slot) awaiting its stores
+    int prev_slot = -1, unit_groups = 0;
     auto signal_prev_all = [&]() {  // producer only: every computed unit complete and counted
         if (prev_slot >= 0) {
             bulk_wait_all();
@@ -1641,40 +1641,49 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, true>::NT, MINB)
     if (producer) {
         const int u0 = atomicAdd(A.ctr, 1);
         s_unit[0] = u0;
+        s_grp[0] = 0;
         s_loaded[0] = 0;
         if (u0 < total && ready(u0)) {
-            load_unit(u0, 0);
+            load_tile(u0, 0, 0);
             s_loaded[0] = 1;
         }
     }
     unsigned uses[2] = {0u, 0u};
     int b = 0;
     for (;;) {
-        __syncthreads();  // s_unit / s_loaded of stage b visible; previous unit's smem reads done
+        __syncthreads();  // stage b's unit / group visible; the previous step's smem reads done
         const int u = s_unit[b];
+        const int gi = s_grp[b];
         if (u >= total) break;
+        int slab, phase, line;
+        decode(u, slab, phase, line);
         if (producer) {
             if (!s_loaded[b]) {
                 signal_prev_all();
                 wait_ready(u);
-                load_unit(u, b);
+                load_tile(u, gi, b);
             }
-            const int nu = atomicAdd(A.ctr, 1);
+            int nu = u, ngi = gi + 1;
+            bool rdy = true;
+            if (ngi >= ng[phase]) {
+                nu = atomicAdd(A.ctr, 1);
+                ngi = 0;
+                rdy = nu < total && ready(nu);
+            }
             s_unit[b ^ 1] = nu;
+            s_grp[b ^ 1] = ngi;
             s_loaded[b ^ 1] = 0;
-            if (nu < total && ready(nu)) {
-                load_unit(nu, b ^ 1);
+            if (nu < total && rdy) {
+                load_tile(nu, ngi, b ^ 1);
                 s_loaded[b ^ 1] = 1;
             }
+            if (gi == 0) unit_groups = 0;
         }
         mbar_wait(&bar[b], uses[b] & 1);
         ++uses[b];
-        int slab, phase, line;
-        decode(u, slab, phase, line);
         const int col0 = slab * TB;
         const PencilJobs& jobs = A.ph[phase];
         float2* xs = xbuf + b * L * TB;
-        int groups = 0;
 
         auto store_tile = [&](int dst) {
             fence_proxy_async_smem();
@@ -1683,8 +1692,8 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, true>::NT, MINB)
 #pragma unroll
                 for (int q = 0; q < NBOX; ++q) box(phase, dst, xs, line, col0, q, false, nullptr);
                 bulk_commit();
+                ++unit_groups;
             }
-            ++groups;
         };
         auto forward = [&](float2 (&X)[N2]) {
             if (inA) {
@@ -1732,81 +1741,54 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, true>::NT, MINB)
             store_tile(dst);
         };
 
+        const int gb = gs[phase][gi], ge = gs[phase][gi + 1];
         float2 X[N2];
         if (phase == 0) {
-            // y forward, every job of the phase is an in-place transform of its own source
-            for (int gi = 0; gi < ng[0]; ++gi) {
-                if (gi > 0) {
-                    // further sources of phase A (the 3-field chain): load synchronously
-                    __syncthreads();
-                    if (producer) {
-                        bulk_wait_read_all();
-                        mbar_arrive_expect_tx(&bar[b], TILE_BYTES);
+            forward(X);
+            if (inB) {
 #pragma unroll
-                        for (int q = 0; q < NBOX; ++q) box(0, jobs.job[gs[0][gi]].src, xs, line, col0, q, true, &bar[b]);
-                    }
-                    mbar_wait(&bar[b], uses[b] & 1);
-                    ++uses[b];
-                }
+                for (int k2 = 0; k2 < N2; ++k2) xs[C::out_row(kb, k2) * TB + c] = X[k2];
+            }
+            store_tile(jobs.job[gb].dst);
+        } else {
+            if (phase == 1) {
                 forward(X);
+                if (inB && jobs.job[gb].kappa) {
+                    if (gi == 0) {  // kappa of the tile, reused by the unit's later source groups
+                        const float ky = g.ky[line];
+                        const float kz = col0 + c < g.nzh ? g.kz[col0 + c] : 0.f;
+                        const float hy = g.half_cdt * ky, hz = g.half_cdt * kz;
+                        const float uyz = hy * hy + hz * hz;
+#pragma unroll
+                        for (int k2 = 0; k2 < N2; ++k2) {
+                            const int k = C::out_row(kb, k2);
+                            kap_s[k * TB + c] = kappa_of_u(hkx2_s[k] + uyz);
+                        }
+                    }
+#pragma unroll
+                    for (int k2 = 0; k2 < N2; ++k2) X[k2] = cscale(X[k2], kap_s[C::out_row(kb, k2) * TB + c]);
+                }
+            } else if (inB) {
+#pragma unroll
+                for (int k2 = 0; k2 < N2; ++k2) X[k2] = xs[C::out_row(kb, k2) * TB + c];
+            }
+            for (int jb = gb; jb < ge; ++jb) {
+                const PencilJob J = jobs.job[jb];
+                float2 bb[N2];
                 if (inB) {
 #pragma unroll
-                    for (int k2 = 0; k2 < N2; ++k2) xs[C::out_row(kb, k2) * TB + c] = X[k2];
+                    for (int k2 = 0; k2 < N2; ++k2)
+                        bb[k2] = J.dmul ? cmul(X[k2], __ldg(J.dmul + C::out_row(kb, k2))) : X[k2];
                 }
-                store_tile(jobs.job[gs[0][gi]].dst);
-            }
-        } else {
-            for (int grp = 0; grp < ng[phase]; ++grp) {
-                const int gb = gs[phase][grp], ge = gs[phase][grp + 1];
-                if (grp > 0) {
-                    __syncthreads();
-                    if (producer) {
-                        bulk_wait_read_all();
-                        mbar_arrive_expect_tx(&bar[b], TILE_BYTES);
-#pragma unroll
-                        for (int q = 0; q < NBOX; ++q) box(phase, jobs.job[gb].src, xs, line, col0, q, true, &bar[b]);
-                    }
-                    mbar_wait(&bar[b], uses[b] & 1);
-                    ++uses[b];
-                }
-                if (phase == 1) {
-                    forward(X);
-                    if (inB && jobs.job[gb].kappa) {
-                        if (grp == 0) {
-                            const float ky = g.ky[line];
-                            const float kz = col0 + c < g.nzh ? g.kz[col0 + c] : 0.f;
-                            const float hy = g.half_cdt * ky, hz = g.half_cdt * kz;
-                            const float uyz = hy * hy + hz * hz;
-#pragma unroll
-                            for (int k2 = 0; k2 < N2; ++k2) {
-                                const int k = C::out_row(kb, k2);
-                                kap_s[k * TB + c] = kappa_of_u(hkx2_s[k] + uyz);
-                            }
-                        }
-#pragma unroll
-                        for (int k2 = 0; k2 < N2; ++k2) X[k2] = cscale(X[k2], kap_s[C::out_row(kb, k2) * TB + c]);
-                    }
-                } else if (inB) {
-#pragma unroll
-                    for (int k2 = 0; k2 < N2; ++k2) X[k2] = xs[C::out_row(kb, k2) * TB + c];
-                }
-                for (int jb = gb; jb < ge; ++jb) {
-                    const PencilJob J = jobs.job[jb];
-                    float2 bb[N2];
-                    if (inB) {
-#pragma unroll
-                        for (int k2 = 0; k2 < N2; ++k2)
-                            bb[k2] = J.dmul ? cmul(X[k2], __ldg(J.dmul + C::out_row(kb, k2))) : X[k2];
-                    }
-                    inverse_store(bb, J.dst);
-                }
+                inverse_store(bb, J.dst);
             }
         }
-        if (producer) {
-            // lazy completion: the previous unit's stores are older than this unit's groups
+        if (producer && gi + 1 == ng[phase]) {
+            // unit done: lazily count the previous unit, whose stores are older than this
+            // unit's store groups
             if (prev_slot >= 0) {
-                if (groups >= 3) bulk_wait_n<3>();
-                else if (groups == 2) bulk_wait_n<2>();
+                if (unit_groups >= 3) bulk_wait_n<3>();
+                else if (unit_groups == 2) bulk_wait_n<2>();
                 else bulk_wait_n<1>();
                 fence_proxy_async_global();
                 __threadfence();
@@ -1837,6 +1819,32 @@ cudaError_t run_chain(const GridDev& g, const PencilJobs& ya, const PencilJobs& 
     a.ctr = ctr;
     a.err = err;
     const int ntx = (g.nzh + TB - 1) / TB;
+    // claim order of the (phase, slab) batches: A0 A1 B0 B1 C0, then (A k, C k-1, B k), then the
+    // last C (see chain_kernel)
+    {
+        std::vector<std::pair<int, int>> order;
+        auto add = [&](int ph, int sl) {
+            if (sl >= 0 && sl < ntx) order.push_back({ph, sl});
+        };
+        add(0, 0);
+        add(0, 1);
+        add(1, 0);
+        add(1, 1);
+        add(2, 0);
+        for (int k = 2; k < ntx; ++k) {
+            add(0, k);
+            add(2, k - 1);
+            add(1, k);
+        }
+        add(2, ntx - 1);
+        if (ntx == 1) order = {{0, 0}, {1, 0}, {2, 0}};
+        if (order.size() != static_cast<size_t>(3 * ntx) || order.size() > sizeof(a.bphase)) return cudaErrorInvalidValue;
+        a.nbatch = static_cast<int>(order.size());
+        for (size_t q = 0; q < order.size(); ++q) {
+            a.bphase[q] = static_cast<unsigned char>(order[q].first);
+            a.bslab[q] = static_cast<unsigned char>(order[q].second);
+        }
+    }
     cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(int) * (1 + 3 * ntx), st);
     if (e != cudaSuccess) return e;
     auto kern = chain_kernel<L, N1, TB, MINB>;

@@ -1,0 +1,100 @@
+"""Parity at the benchmarked inputs, against fixtures the REFERENCE itself
+produced (oracle/_ref, tests/golden/make_golden_large.py; hours of fp64 CPU work each):
+
+  config B, full nt = 961: the 128^3 breast phantom, 64 Rademacher-encoded emitters (realization
+      0 of master seed 20210201), 64 receivers, shell thickness 8 — forward traces and shell-trace
+      checksums, loss and the Gamma-restricted TR gradient;
+  config D grid, nt = 160: the bench's own 480x480x256 phantom with 1024 encoded emitters and
+      1024 receivers — the 480-point pencils, the nz = 256 rows, the 1.16 M-voxel shell: traces,
+      per-step shell-trace sums;
+  fp32 drift, config A geometry at nt = 3912 (the config-D step count): traces and TR gradient
+      after 3 * 3912 - 3 steps.
+
+Bars (BASELINE.json north_star): traces rel l2 <= 1e-4, gradient rel l2 <= 1e-3."""
+import numpy as np
+import pytest
+
+from paper_2102_00755_b200 import scenario
+from paper_2102_00755_b200.engine import GpuEngine
+
+pytestmark = pytest.mark.gpu
+
+TRACE_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - np.asarray(b, np.float64)) /
+                 np.linalg.norm(np.asarray(b, np.float64)))
+
+
+def load(golden, name):
+    try:
+        return golden(name)
+    except FileNotFoundError:
+        pytest.skip(f"{name} fixture not generated (tests/golden/make_golden_large.py)")
+
+
+def gradient_parity(sc, z):
+    enc = sc.encoded(0)
+    assert np.array_equal(np.asarray(enc.weights, np.float64), z["weights"])  # identical encoding sequence
+    with GpuEngine(sc.grid) as eng:
+        eng.set_medium(sc.model)
+        eng.set_sources(enc)
+        eng.set_sensors(sc.sensors)
+        data, trace = eng.forward(sc.thickness)
+        loss, grad = eng.gradient_tr(z["observed"], sc.thickness)
+    res = {"traces": rel(data, z["data_model"]), "loss": abs(loss - float(z["loss"])) / float(z["loss"]),
+           "grad": rel(grad.ravel()[z["gamma_idx"]], z["grad_gamma"])}
+    t = np.asarray(trace, np.float64)
+    want = z["trace_checksum"]
+    res["trace_sum"] = abs(t.sum() - want[0]) / abs(want[1])
+    res["trace_abs"] = abs(np.abs(t).sum() - want[1]) / want[1]
+    res["trace_sq"] = abs((t ** 2).sum() - want[2]) / want[2]
+    res["grad_outside"] = float(np.abs(np.delete(grad.ravel(), z["gamma_idx"])).max())
+    return res
+
+
+def test_config_b_full_nt_matches_reference(golden):
+    z = load(golden, "config_b")
+    sc = scenario.config_b()
+    assert sc.grid.nt == int(z["nt"]) == 961
+    r = gradient_parity(sc, z)
+    print("config B:", r)
+    assert r["traces"] < TRACE_TOL
+    assert r["trace_abs"] < TRACE_TOL and r["trace_sq"] < 2 * TRACE_TOL and r["trace_sum"] < TRACE_TOL
+    assert r["loss"] < TRACE_TOL
+    assert r["grad"] < GRAD_TOL and r["grad_outside"] == 0.0
+
+
+def test_fp32_drift_over_3912_steps(golden):
+    z = load(golden, "config_a_nt3912")
+    sc = scenario.config_a(nt=3912)
+    r = gradient_parity(sc, z)
+    print("config A at nt 3912 (fp32 drift over 11733 steps):", r)
+    assert r["traces"] < TRACE_TOL and r["loss"] < TRACE_TOL
+    assert r["grad"] < GRAD_TOL
+
+
+def test_config_d_grid_forward_matches_reference(golden):
+    z = load(golden, "config_d_short")
+    sc = scenario.config_d(nt=int(z["nt"]))
+    enc = sc.encoded(0)
+    assert np.array_equal(np.asarray(enc.weights, np.float64), z["weights"])
+    with GpuEngine(sc.grid) as eng:
+        eng.set_medium(sc.model)
+        eng.set_sources(enc)
+        eng.set_sensors(sc.sensors)
+        data, trace = eng.forward(sc.thickness)
+    t = np.asarray(trace, np.float64)
+    assert t.shape[1] == int(z["n_shell"])
+    r_traces = rel(data, z["data_model"])
+    r_steps = rel(t.sum(axis=1), z["trace_step_sum"])
+    r_steps_abs = rel(np.abs(t).sum(axis=1), z["trace_step_abs"])
+    st = z["trace_stride"]
+    r_sub = rel(t[::st[0], ::st[1]], z["trace_sub"])
+    print(f"config D grid nt {sc.grid.nt}: traces {r_traces:.2e}, shell per-step sums {r_steps:.2e} / "
+          f"abs {r_steps_abs:.2e}, subsample {r_sub:.2e}")
+    assert r_traces < TRACE_TOL
+    assert r_steps_abs < TRACE_TOL and r_sub < TRACE_TOL
+    assert r_steps < 10 * TRACE_TOL   # signed sums cancel: looser relative bar
