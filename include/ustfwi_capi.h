@@ -227,6 +227,10 @@ USTFWI_API size_t ustfwi_gpu_shell_size(const ustfwi_gpu_ctx* ctx);
 #define USTFWI_KERNEL_AUX 4
 #define USTFWI_KERNEL_CHAIN 5 /* fused y-x-y chain (y forward, x * kappa * D_x * inverse, y inverse) */
 #define USTFWI_KERNEL_KINDS 6
+/* Fused y-x-y chain kernel wait statistics (only with USTFWI_CHAIN_STATS=1; diagnostics):
+ * out[0] CTAs, out[1] units, out[2] deferred tile loads, out[3] dependency-wait cycles,
+ * out[4] tile-wait cycles, summed over CTAs since the previous call. */
+USTFWI_API int ustfwi_gpu_chain_stats(uint64_t* out5);
 /* Enable/disable event timing of every launch and reset the counters. */
 USTFWI_API int ustfwi_gpu_set_profiling(ustfwi_gpu_ctx* ctx, int enable);
 /* Accumulated device time, launch count and algorithmic bytes (minimum HBM traffic of the

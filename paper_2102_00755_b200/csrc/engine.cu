@@ -1915,6 +1915,17 @@ int ustfwi_gpu_kernel_stats(ustfwi_gpu_ctx* c, int kind, double* total_ms, uint6
     });
 }
 
+// diagnostics of the fused y-x-y chain kernel (USTFWI_CHAIN_STATS=1): CTAs, units, deferred
+// (blocking) tile loads, cycles spent waiting for dependencies and for tiles, summed over CTAs
+int ustfwi_gpu_chain_stats(uint64_t* out5) {
+    return guarded(nullptr, [&] {
+        unsigned long long t[4];
+        const int n = chain_stats(t);
+        out5[0] = static_cast<uint64_t>(n);
+        for (int k = 0; k < 4; ++k) out5[k + 1] = t[k];
+    });
+}
+
 int ustfwi_nccl_unique_id(char id_out[128]) {
     return guarded(nullptr, [&] {
         NcclUniqueId id;

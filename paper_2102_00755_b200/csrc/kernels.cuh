@@ -263,6 +263,7 @@ cudaError_t launch_zvel_fast(const GridDev& g, float2* S[3], const float2* dz_pl
 cudaError_t launch_zrho_fast(const GridDev& g, const ZrhoArgs& a, cudaStream_t st);
 bool use_generic_kernels();
 bool chain_supported(const GridDev& g);
+int chain_stats(unsigned long long out[4]);
 cudaError_t launch_chain(const GridDev& g, const PencilJobs& ya, const PencilJobs& xb, const PencilJobs& yc, int* ctr,
                          int* err, cudaStream_t st);
 

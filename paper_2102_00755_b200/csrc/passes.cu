@@ -1523,6 +1523,8 @@ struct ChainArgs {
     int* err;           // set on a dependency-wait timeout
     int nbatch;         // claim order: batch q = (phase, slab) of `lines` consecutive units
     unsigned char bphase[64], bslab[64];
+    int eager;                      // signal every unit as soon as its stores landed
+    unsigned long long* stats;      // per CTA: [units, deferred loads, wait cycles, mbar cycles]
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -1627,7 +1629,9 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, true>::NT, MINB)
             prev_slot = -1;
         }
     };
+    unsigned long long st_units = 0, st_def = 0, st_wait = 0, st_mbar = 0;
     auto wait_ready = [&](int u) {  // producer only, blocking (bounded)
+        const unsigned long long t0 = clock64();
         unsigned spins = 0;
         while (!ready(u)) {
             __nanosleep(64);
@@ -1636,6 +1640,7 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, true>::NT, MINB)
                 break;
             }
         }
+        st_wait += clock64() - t0;
     };
 
     if (producer) {
@@ -1659,6 +1664,7 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, true>::NT, MINB)
         decode(u, slab, phase, line);
         if (producer) {
             if (!s_loaded[b]) {
+                ++st_def;
                 signal_prev_all();
                 wait_ready(u);
                 load_tile(u, gi, b);
@@ -1679,7 +1685,11 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, true>::NT, MINB)
             }
             if (gi == 0) unit_groups = 0;
         }
-        mbar_wait(&bar[b], uses[b] & 1);
+        {
+            const unsigned long long t0 = A.stats ? clock64() : 0ull;
+            mbar_wait(&bar[b], uses[b] & 1);
+            if (A.stats && producer) st_mbar += clock64() - t0;
+        }
         ++uses[b];
         const int col0 = slab * TB;
         const PencilJobs& jobs = A.ph[phase];
@@ -1784,9 +1794,14 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, true>::NT, MINB)
             }
         }
         if (producer && gi + 1 == ng[phase]) {
+            ++st_units;
+            if (A.eager) {
+                prev_slot = 1 + 3 * slab + phase;
+                signal_prev_all();
+            }
             // unit done: lazily count the previous unit, whose stores are older than this
             // unit's store groups
-            if (prev_slot >= 0) {
+            else if (prev_slot >= 0) {
                 if (unit_groups >= 3) bulk_wait_n<3>();
                 else if (unit_groups == 2) bulk_wait_n<2>();
                 else bulk_wait_n<1>();
@@ -1794,11 +1809,37 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, true>::NT, MINB)
                 __threadfence();
                 atomicAdd(A.ctr + prev_slot, 1);
             }
-            prev_slot = 1 + 3 * slab + phase;
+            if (!A.eager) prev_slot = 1 + 3 * slab + phase;
         }
         b ^= 1;
     }
-    if (producer) signal_prev_all();
+    if (producer) {
+        signal_prev_all();
+        if (A.stats) {
+            unsigned long long* o = A.stats + 4 * blockIdx.x;
+            o[0] += st_units;
+            o[1] += st_def;
+            o[2] += st_wait;
+            o[3] += st_mbar;
+        }
+    }
+}
+
+// USTFWI_CHAIN_STATS=1: per-CTA wait statistics of the chain kernel (diagnostics)
+unsigned long long* g_chain_stats = nullptr;
+int g_chain_stats_n = 0;
+unsigned long long* chain_stats_buffer(int nctas) {
+    static const bool on = [] {
+        const char* e = std::getenv("USTFWI_CHAIN_STATS");
+        return e && e[0] == '1';
+    }();
+    if (!on) return nullptr;
+    if (!g_chain_stats) {
+        if (cudaMalloc(&g_chain_stats, sizeof(unsigned long long) * 4 * nctas) != cudaSuccess) return nullptr;
+        cudaMemset(g_chain_stats, 0, sizeof(unsigned long long) * 4 * nctas);
+        g_chain_stats_n = nctas;
+    }
+    return g_chain_stats;
 }
 
 template <int L, int N1, int TB, int MINB>
@@ -1818,6 +1859,12 @@ cudaError_t run_chain(const GridDev& g, const PencilJobs& ya, const PencilJobs& 
         }
     a.ctr = ctr;
     a.err = err;
+    static const int eager = [] {
+        const char* e = std::getenv("USTFWI_CHAIN_EAGER");
+        return e ? std::atoi(e) : 0;
+    }();
+    a.eager = eager;
+    a.stats = chain_stats_buffer(sm_count() * MINB);
     const int ntx = (g.nzh + TB - 1) / TB;
     // claim order of the (phase, slab) batches: A0 A1 B0 B1 C0, then (A k, C k-1, B k), then the
     // last C (see chain_kernel)
@@ -1826,18 +1873,52 @@ cudaError_t run_chain(const GridDev& g, const PencilJobs& ya, const PencilJobs& 
         auto add = [&](int ph, int sl) {
             if (sl >= 0 && sl < ntx) order.push_back({ph, sl});
         };
-        add(0, 0);
-        add(0, 1);
-        add(1, 0);
-        add(1, 1);
-        add(2, 0);
-        for (int k = 2; k < ntx; ++k) {
-            add(0, k);
-            add(2, k - 1);
-            add(1, k);
+        static const int mode = [] {
+            const char* e = std::getenv("USTFWI_CHAIN_ORDER");
+            return e ? std::atoi(e) : 0;
+        }();
+        if (mode == 1) {  // plain slab-major
+            for (int k = 0; k < ntx; ++k) {
+                add(0, k);
+                add(1, k);
+                add(2, k);
+            }
+        } else if (mode == 2) {  // wider gaps: A0 A1 A2 B0 B1 C0, then (A k, C k-2, B k-1), tail
+            add(0, 0);
+            add(0, 1);
+            add(0, 2);
+            add(1, 0);
+            add(1, 1);
+            add(2, 0);
+            for (int k = 3; k < ntx; ++k) {
+                add(0, k);
+                add(2, k - 2);
+                add(1, k - 1);
+            }
+            add(2, ntx - 2);
+            add(1, ntx - 1);
+            add(2, ntx - 1);
+        } else {
+            add(0, 0);
+            add(0, 1);
+            add(1, 0);
+            add(1, 1);
+            add(2, 0);
+            for (int k = 2; k < ntx; ++k) {
+                add(0, k);
+                add(2, k - 1);
+                add(1, k);
+            }
+            add(2, ntx - 1);
         }
-        add(2, ntx - 1);
-        if (ntx == 1) order = {{0, 0}, {1, 0}, {2, 0}};
+        if (ntx < 4) {
+            order.clear();
+            for (int k = 0; k < ntx; ++k) {
+                add(0, k);
+                add(1, k);
+                add(2, k);
+            }
+        }
         if (order.size() != static_cast<size_t>(3 * ntx) || order.size() > sizeof(a.bphase)) return cudaErrorInvalidValue;
         a.nbatch = static_cast<int>(order.size());
         for (size_t q = 0; q < order.size(); ++q) {
@@ -1920,6 +2001,18 @@ cudaError_t launch_chain(const GridDev& g, const PencilJobs& ya, const PencilJob
                          int* err, cudaStream_t st) {
     if (!chain_supported(g)) return cudaErrorInvalidValue;
     return run_chain<480, 30, 8, 2>(g, ya, xb, yc, ctr, err, st);
+}
+
+// totals of the chain-kernel wait statistics since the last call (USTFWI_CHAIN_STATS=1)
+int chain_stats(unsigned long long out[4]) {
+    for (int k = 0; k < 4; ++k) out[k] = 0;
+    if (!g_chain_stats) return 0;
+    std::vector<unsigned long long> h(4 * static_cast<size_t>(g_chain_stats_n));
+    cudaDeviceSynchronize();
+    cudaMemcpy(h.data(), g_chain_stats, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaMemset(g_chain_stats, 0, h.size() * sizeof(unsigned long long));
+    for (size_t i = 0; i < h.size(); ++i) out[i % 4] += h[i];
+    return g_chain_stats_n;
 }
 
 bool fast_rows_supported(int nz) {
