@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -1472,6 +1473,12 @@ cudaError_t run_pencil_tma(const GridDev& g, const PencilJobs& j, cudaStream_t s
     });
     const int ntiles = ((g.nzh + TB - 1) / TB) * (AXIS == 0 ? g.ny : g.xn);
     const int grid = (!DB || ntiles < sm_count() * MINB) ? ntiles : sm_count() * MINB;
+    static int occ = -1;
+    if (occ < 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT, smem);
+        if (std::getenv("USTFWI_CHAIN_STATS"))
+            fprintf(stderr, "pencil_tma_kernel<%d,%d,%d>: %d CTAs per SM (smem %zu B)\n", AXIS, (int)INV, L, occ, smem);
+    }
     kern<<<grid, C::NT, smem, st>>>(g, j, maps);
     return cudaGetLastError();
 }
@@ -1933,7 +1940,12 @@ cudaError_t run_chain(const GridDev& g, const PencilJobs& ya, const PencilJobs& 
                             size_t(L) * (TB + 1) * sizeof(float);
     static std::atomic<unsigned long long> configured{0};
     once_per_device(configured, [&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
-    kern<<<sm_count() * MINB, C::NT, smem, st>>>(g, a);
+    static int occ = -1;
+    if (occ < 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT, smem);
+        if (a.stats) fprintf(stderr, "chain_kernel: %d CTAs per SM (smem %zu B, %d threads)\n", occ, smem, C::NT);
+    }
+    kern<<<sm_count() * (occ > 0 ? std::min(occ, MINB) : MINB), C::NT, smem, st>>>(g, a);
     return cudaGetLastError();
 }
 #endif  // !USTFWI_PASSES_Y_ONLY

@@ -2,8 +2,9 @@
 z kernels, USTFWI_GENERIC=1: runtime-plan Stockham kernels, USTFWI_X480=1: 32x15 x pass)
 compute the same step: forward traces of a grid that selects the 480-point y pencils and
 the nz = 256 z kernels agree across variants (each variant in its own process, the switches
-are read once). On a 480 x 480 x 32 grid the fused y-x-y chain kernel (default) and the three
-separate pencil launches (USTFWI_CHAIN=0) give the same traces and TR gradient."""
+are read once). On a 480 x 480 x 32 grid the three separate pencil launches (default) and the
+experimental fused y-x-y chain kernel (USTFWI_CHAIN=1) give the same traces and TR gradient,
+and the eager launches (USTFWI_GRAPH=0) the same as the CUDA-graph replay."""
 import json
 import os
 import subprocess
@@ -59,7 +60,7 @@ def run(env_extra, layout):
 @pytest.mark.parametrize("layout,variant", [
     ("y", {"USTFWI_PENCIL_TMA": "0"}), ("y", {"USTFWI_ZROW2": "0"}), ("y", {"USTFWI_GENERIC": "1"}),
     ("x", {"USTFWI_X480": "1"}), ("x", {"USTFWI_PENCIL_TMA": "0"}),
-    ("xy", {"USTFWI_CHAIN": "0"}), ("xy", {"USTFWI_GRAPH": "0"}),
+    ("xy", {"USTFWI_CHAIN": "1"}), ("xy", {"USTFWI_GRAPH": "0"}),
 ])
 def test_kernel_variants_agree(layout, variant):
     base = run({}, layout)
