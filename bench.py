@@ -109,7 +109,8 @@ class ClockSampler:
 # interior, dx (m), emitters, nt override (the paper's nt at D); the grid itself
 # comes from the reference's own make_grid (grid.hpp:91-103) through oracle/_ref
 CONFIG_SPECS = {"A": ([44, 44, 44], 1e-3, 1, None), "B": ([108, 108, 108], 1e-3, 64, None),
-                "C": ([236, 236, 236], 1e-3, 256, None), "D": ([442, 442, 222], 0.5e-3, 1024, 3912)}
+                "C": ([236, 236, 236], 1e-3, 256, None), "D": ([442, 442, 222], 0.5e-3, 1024, 3912),
+                "E0": ([112, 112, 56], 2e-3, 64, 978), "E1": ([222, 222, 112], 1e-3, 256, 1956)}
 # resident fp64 bytes per grid point of one ref_time_steps process: engine multipliers and
 # spectra + three steppers + accumulator (measured here: 23.7 GB for a D forward with its
 # shell trace; SURVEY §8(d) estimates 28 GiB for a TR gradient) -> 64 doubles per point
@@ -491,7 +492,7 @@ def main():
     p.add_argument("--steps", type=int, default=2)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default="D", choices=["A", "B", "C", "D"])
+    p.add_argument("--config", default="D", choices=["A", "B", "C", "D", "E0", "E1"])
     p.add_argument("--e2e-steps", type=int, default=1)
     p.add_argument("--cpu-baseline", type=int, default=1)
     p.add_argument("--batch", type=int, default=0,

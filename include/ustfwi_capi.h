@@ -265,9 +265,10 @@ USTFWI_API int ustfwi_lbfgs_destroy(ustfwi_lbfgs* h);
 /* Forget all pairs (H0 = I). */
 USTFWI_API int ustfwi_lbfgs_reset(ustfwi_lbfgs* h);
 /* updateBuffer(s, S), updateBuffer(y, Y) (Algorithm 2); the pair is rejected (*accepted = 0)
- * unless <s,y> > reject_tol * |s| |y| (SPEC design decision, default 1e-10). Host vectors. */
+ * unless <s,y> > reject_tol * |s| |y| (SPEC design decision, default 1e-10). Host or device
+ * vectors (unified addressing; device vectors stay in HBM). */
 USTFWI_API int ustfwi_lbfgs_push(ustfwi_lbfgs* h, const double* s, const double* y, double reject_tol, int* accepted);
-/* out = H_k g by the two-loop recursion (empty history: g). Host vectors. */
+/* out = H_k g by the two-loop recursion (empty history: g). Host or device vectors. */
 USTFWI_API int ustfwi_lbfgs_apply(ustfwi_lbfgs* h, const double* g, double* out);
 /* Number of stored pairs and the current H0 scaling. */
 USTFWI_API int ustfwi_lbfgs_pairs(const ustfwi_lbfgs* h, int* count, double* gamma);

@@ -227,8 +227,9 @@ USTFWI_API int ustfwi_lbfgs_push(ustfwi_lbfgs* h, const double* s, const double*
         // stage in the work vectors: a rejected pair must not clobber the oldest stored one
         double* sk = h->q;
         double* yk = h->r;
-        LCK(cudaMemcpyAsync(sk, s, h->n * sizeof(double), cudaMemcpyHostToDevice, h->st));
-        LCK(cudaMemcpyAsync(yk, y, h->n * sizeof(double), cudaMemcpyHostToDevice, h->st));
+        // s, y: host or device pointers (unified addressing)
+        LCK(cudaMemcpyAsync(sk, s, h->n * sizeof(double), cudaMemcpyDefault, h->st));
+        LCK(cudaMemcpyAsync(yk, y, h->n * sizeof(double), cudaMemcpyDefault, h->st));
         const double sy = h->dot_host(sk, yk);
         const double ss = h->dot_host(sk, sk);
         const double yy = h->dot_host(yk, yk);
@@ -253,9 +254,11 @@ USTFWI_API int ustfwi_lbfgs_push(ustfwi_lbfgs* h, const double* s, const double*
 USTFWI_API int ustfwi_lbfgs_apply(ustfwi_lbfgs* h, const double* g, double* out) {
     return lguard(h, [&] {
         if (!h || !g || !out) throw Fail{USTFWI_ERR_INVALID, "null argument"};
-        LCK(cudaMemcpyAsync(h->r, g, h->n * sizeof(double), cudaMemcpyHostToDevice, h->st));
+        // g, out: host or device pointers (unified addressing): with device vectors the
+        // recursion never leaves HBM
+        LCK(cudaMemcpyAsync(h->r, g, h->n * sizeof(double), cudaMemcpyDefault, h->st));
         h->two_loop(h->r);
-        LCK(cudaMemcpyAsync(out, h->r, h->n * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        LCK(cudaMemcpyAsync(out, h->r, h->n * sizeof(double), cudaMemcpyDefault, h->st));
         LCK(cudaStreamSynchronize(h->st));
     });
 }

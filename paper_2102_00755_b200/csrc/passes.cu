@@ -2046,6 +2046,18 @@ bool use_zrow2() {
     return on == 1;
 }
 
+// smallest half length M = nz / 2 that takes the paired-residue rows: velocity (kind 0) and
+// density / pressure (kind 1) passes; USTFWI_ZROW2_MIN="<vel>,<rho>" overrides (measurement)
+int zrow2_min(int kind) {
+    static int v[2] = {-1, -1};
+    if (v[0] < 0) {
+        v[0] = 64;
+        v[1] = 128;
+        if (const char* e = std::getenv("USTFWI_ZROW2_MIN")) std::sscanf(e, "%d,%d", &v[0], &v[1]);
+    }
+    return v[kind];
+}
+
 template <int M, int N1, int RW>
 cudaError_t zvel2_run(const GridDev& g, const ZvelFastArgs& a, cudaStream_t st) {
     const size_t smem = Z2Smem<M, N1, RW>::bytes(g.nzp, a.r[0].field ? 2 : 1);
@@ -2103,7 +2115,7 @@ cudaError_t zvel_sized(const GridDev& g, float2* S[3], const float2* dz_plus, fl
     // paired-residue rows where they win on B200: z-vel for M >= 64 (config B 0.036 -> 0.027 ms,
     // D 0.80 -> 0.54 ms), the density/pressure pair for M >= 128 only (config A/B: the
     // 8-row kernels are faster, 0.037 vs 0.062 ms at A)
-    if (M >= 64 && use_zrow2()) return zvel2_sized<M>(g, a, st);
+    if (M >= zrow2_min(0) && use_zrow2()) return zvel2_sized<M>(g, a, st);
     const size_t smem = C::FIXED + size_t(kZRows) * g.nzp * 8 + size_t(r[0].field ? 2 : 1) * kZRows * C::NZ * 4;
     auto kern = zvel_fast_kernel<M, N1, kZRows>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -2119,7 +2131,7 @@ cudaError_t zrho_sized(const GridDev& g, const ZrhoArgs& za, cudaStream_t st) {
     a.a = za;
     const unsigned blocks = (unsigned)(((long long)g.xn * g.ny + kZRows - 1) / kZRows);
     // density update, one CTA per (row block, axis)
-    if (M >= 128 && use_zrow2()) return zrho2_sized<M>(g, a, st);
+    if (M >= zrow2_min(1) && use_zrow2()) return zrho2_sized<M>(g, a, st);
     {
     const size_t smem1 = 16 + size_t(M) * 8 + size_t(kZRows) * C::ZT * 8 + size_t(kZRows) * g.nzp * 8 +
                          size_t(za.dtrho0.field ? 2 : 1) * kZRows * C::NZ * 4;

@@ -4,8 +4,9 @@ module).
 
 The curvature history (S, Y rings of m_h = 64 fp64 vectors, rho_i, H0 = gamma I) lives on
 the device behind the C ABI (`ustfwi_lbfgs_*`, csrc/lbfgs.cu); the two-loop recursion runs
-there. The iterate bookkeeping (projection, averaging, energy history) is host-side numpy,
-as cheap next to one gradient evaluation.
+there. The iterate bookkeeping (projection, averaging, energy history) runs on whatever the
+caller's vectors are: numpy arrays (host) or torch CUDA fp64 tensors, in which case every
+vector of Algorithm 2 stays in HBM (push / apply pass device pointers, no transfers).
 
 Estimator contract (Algorithm 2 inputs): ``estimator(u, theta, n) -> (F, G)`` where the same
 ``(theta, n)`` selects the same stochastic approximation (seed pairing).
@@ -22,6 +23,40 @@ import numpy as np
 from .capi import check, lib, ptr
 
 Estimator = Callable[[np.ndarray, float, int], Tuple[float, np.ndarray]]
+
+
+def _is_cuda(x) -> bool:
+    return type(x).__module__.split(".")[0] == "torch" and bool(getattr(x, "is_cuda", False))
+
+
+class _Np:
+    """Vector ops of Algorithm 2 on numpy (host)."""
+    @staticmethod
+    def vec(x, shape):
+        return np.asarray(x, dtype=np.float64).reshape(shape)
+
+    copy = staticmethod(lambda x: np.array(x, dtype=np.float64, copy=True))
+    zeros_like = staticmethod(np.zeros_like)
+    norm = staticmethod(lambda x: float(np.linalg.norm(x)))
+    dot = staticmethod(lambda a, b: float(np.dot(a.ravel(), b.ravel())))
+    clip = staticmethod(lambda u, lo, hi: np.maximum(np.minimum(u, hi), lo))
+
+
+class _Torch:
+    """The same ops on torch CUDA fp64 tensors (device-resident iterates)."""
+    @staticmethod
+    def vec(x, shape):
+        return x.to(dtype=__import__("torch").float64).reshape(shape)
+
+    copy = staticmethod(lambda x: x.detach().clone().to(dtype=__import__("torch").float64))
+    zeros_like = staticmethod(lambda x: __import__("torch").zeros_like(x))
+    norm = staticmethod(lambda x: float(__import__("torch").linalg.vector_norm(x)))
+    dot = staticmethod(lambda a, b: float(__import__("torch").dot(a.reshape(-1), b.reshape(-1))))
+    clip = staticmethod(lambda u, lo, hi: __import__("torch").clamp(u, lo, hi))
+
+
+def _ops(x):
+    return _Torch if _is_cuda(x) else _Np
 
 
 class DeviceLbfgs:
@@ -60,7 +95,19 @@ class DeviceLbfgs:
         check(lib().ustfwi_lbfgs_reset(self._h))
 
     def push(self, s: np.ndarray, y: np.ndarray) -> bool:
-        """updateBuffer(s, S), updateBuffer(y, Y); False when the curvature pair is rejected."""
+        """updateBuffer(s, S), updateBuffer(y, Y); False when the curvature pair is rejected.
+        Host arrays or torch CUDA tensors (device pointers, no transfer)."""
+        if _is_cuda(s):
+            import torch
+            s = s.detach().to(torch.float64).contiguous().reshape(-1)
+            y = y.detach().to(torch.float64).contiguous().reshape(-1)
+            if s.numel() != self.n or y.numel() != self.n:
+                raise ValueError("pair length does not match the state")
+            torch.cuda.current_stream(s.device).synchronize()
+            ok = C.c_int(0)
+            check(lib().ustfwi_lbfgs_push(self._h, C.c_void_p(s.data_ptr()), C.c_void_p(y.data_ptr()),
+                                          self.reject_tol, C.byref(ok)))
+            return bool(ok.value)
         s = np.ascontiguousarray(s, dtype=np.float64).ravel()
         y = np.ascontiguousarray(y, dtype=np.float64).ravel()
         if s.size != self.n or y.size != self.n:
@@ -71,7 +118,17 @@ class DeviceLbfgs:
         return bool(ok.value)
 
     def apply(self, g: np.ndarray) -> np.ndarray:
-        """H_k g by the two-loop recursion (Algorithm 2 twoLoopRecursion)."""
+        """H_k g by the two-loop recursion (Algorithm 2 twoLoopRecursion); a torch CUDA tensor
+        in gives a torch CUDA tensor out (device pointers, no transfer)."""
+        if _is_cuda(g):
+            import torch
+            gd = g.detach().to(torch.float64).contiguous().reshape(-1)
+            if gd.numel() != self.n:
+                raise ValueError("vector length does not match the state")
+            out = torch.empty_like(gd)
+            torch.cuda.current_stream(gd.device).synchronize()
+            check(lib().ustfwi_lbfgs_apply(self._h, C.c_void_p(gd.data_ptr()), C.c_void_p(out.data_ptr())))
+            return out
         g = np.ascontiguousarray(g, dtype=np.float64).ravel()
         if g.size != self.n:
             raise ValueError("vector length does not match the state")
@@ -100,14 +157,14 @@ def _project(u, bounds):
     if bounds is None:
         return u
     lo, hi = bounds
-    return np.maximum(np.minimum(u, hi), lo)
+    return _ops(u).clip(u, lo, hi)
 
 
 def line_search(f: Callable[[np.ndarray], Tuple[float, np.ndarray]], u: np.ndarray, z: np.ndarray, nu0: float,
                 F0: float, G0: np.ndarray, c1: float = 1e-4, max_trials: int = 8):
     """Backtracking Armijo search (SPEC.md optimizer line_search): halving from nu0, at most
     8 trials. Returns (F, G, nu, evals, ok)."""
-    slope = float(np.dot(G0.ravel(), z.ravel()))
+    slope = _ops(z).dot(G0, z)
     if not slope < 0.0:
         F, G = f(u + nu0 * z)
         return F, G, nu0, 1, False
@@ -133,19 +190,21 @@ def slbfgs_run(estimator: Estimator, u0: np.ndarray, n_evl: int, nu: float = 1.0
     gamma = <s,y>/<y,y> scaling of the newest pair. The step size nu multiplies
     both updates, so with gradients not in parameter units keep nu = 1 and put the scale of
     the first step into h0."""
-    u = np.array(u0, dtype=np.float64, copy=True)
-    shape = u.shape
-    u_bar = np.zeros_like(u)
+    X = _ops(u0)
+    u = X.copy(u0)
+    shape = tuple(u.shape)
+    u_bar = X.zeros_like(u)
     w_bar = 0.0
     J_prev = math.inf
     energy: List[float] = []
     log: List[dict] = []
     average = False
     avg_from = None
-    u_hat = u.copy()
+    u_hat = X.copy(u)
     evl = 0
     i = 0
-    with DeviceLbfgs(u.size, history, device, reject_tol) as H:
+    n = int(np.prod(shape)) if shape else 1
+    with DeviceLbfgs(n, history, device, reject_tol) as H:
         def apply_h(g):
             r = H.apply(g).reshape(shape)
             return h0 * r if H.pairs()[0] == 0 else r
@@ -155,7 +214,7 @@ def slbfgs_run(estimator: Estimator, u0: np.ndarray, n_evl: int, nu: float = 1.0
             th = theta(i)
             F_u, G_u = estimator(u, th, i)
             evl += 1
-            G_u = np.asarray(G_u, dtype=np.float64).reshape(shape)
+            G_u = X.vec(G_u, shape)
             z = -apply_h(G_u)
             step = nu
             if do_linesearch:
@@ -164,7 +223,7 @@ def slbfgs_run(estimator: Estimator, u0: np.ndarray, n_evl: int, nu: float = 1.0
                 F_z, G_z = estimator(u + nu * z, th, i)
                 m_evl = 1
             evl += m_evl
-            G_z = np.asarray(G_z, dtype=np.float64).reshape(shape)
+            G_z = X.vec(G_z, shape)
             accepted = H.push(step * z, G_z - G_u)
             z = z - apply_h(G_z)
             u = _project(u + step * z, bounds)
@@ -179,10 +238,10 @@ def slbfgs_run(estimator: Estimator, u0: np.ndarray, n_evl: int, nu: float = 1.0
                 if J > J_prev:
                     average = True
                     avg_from = i + 1
-                u_hat = u.copy()
+                u_hat = X.copy(u)
             J_prev = J
-            log.append({"iter": i, "n_evl": evl, "J": J, "step_norm": float(np.linalg.norm(step * z)),
-                        "grad_norm": float(np.linalg.norm(G_u)), "averaging_active": average,
+            log.append({"iter": i, "n_evl": evl, "J": J, "step_norm": X.norm(step * z),
+                        "grad_norm": X.norm(G_u), "averaging_active": average,
                         "pair_accepted": accepted})
     return OptResult(u_hat, energy, evl, i, avg_from, log)
 

@@ -248,4 +248,5 @@ def encoding_problem(n_src: int, nt: Optional[int] = None):
     return g, model, truth, srcs, sens, pulse
 
 
-CONFIGS = {"A": config_a, "B": config_b, "C": config_c, "D": config_d}
+CONFIGS = {"A": config_a, "B": config_b, "C": config_c, "D": config_d,
+           "E0": lambda nt=None: config_e(0, nt), "E1": lambda nt=None: config_e(1, nt)}

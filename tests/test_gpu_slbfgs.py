@@ -144,3 +144,23 @@ def test_slbfgs_drives_the_tr_gradient_engine():
     # the first trial step along -G (H0 = I) decreases the data misfit: J_1 = min(F_u, F_z) < F_u
     assert res.energy[0] < F0
     assert res.log[0]["pair_accepted"]
+
+
+def test_slbfgs_device_resident_vectors_match_host():
+    # the same Algorithm 2 run with torch CUDA fp64 iterates (push / apply on device pointers,
+    # no transfers) and with numpy host iterates
+    import torch
+    A, b, ustar = _quadratic(3, 200)
+    At, bt = torch.tensor(A, device="cuda"), torch.tensor(b, device="cuda")
+
+    def est_h(u, th, k):
+        return 0.5 * u @ A @ u - b @ u, A @ u - b
+
+    def est_d(u, th, k):
+        return float(0.5 * u @ (At @ u) - bt @ u), At @ u - bt
+
+    rh = slbfgs_run(est_h, np.zeros(200), 40, nu=0.5)
+    rd = slbfgs_run(est_d, torch.zeros(200, dtype=torch.float64, device="cuda"), 40, nu=0.5)
+    assert torch.is_tensor(rd.u) and rd.u.is_cuda
+    assert np.allclose(rh.energy, rd.energy, rtol=1e-9, atol=1e-13)
+    assert np.linalg.norm(rd.u.cpu().numpy() - rh.u) <= 1e-9 * np.linalg.norm(rh.u)
