@@ -50,6 +50,7 @@ struct Sim {
     float2* S[3] = {};
     bool pml_off = false;   // StepperOptions::pml_enabled == false (engine.hpp:171,202-213)
     int* chain_ctr = nullptr;  // claim / completion counters of this simulation's chain kernel
+    int pgrid = 0;             // persistent pencil grid of this simulation's passes (0: default)
 };
 
 // WaveStepper options and counters of the step-level C ABI (engine.hpp:170-177,344-346)
@@ -135,6 +136,7 @@ struct ustfwi_gpu_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr;   // time-reversal replay stream of the pair loop
     cudaEvent_t ev_adj[2] = {}, ev_rep[2] = {}, ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_lag[8] = {};       // pair-loop phase shift (USTFWI_PAIR_LAG)
     float* adj_p2 = nullptr;          // second adjoint pressure buffer (pair loop)
     uint64_t launches = 0;
     ustfwi_grid grid{};
@@ -397,6 +399,10 @@ struct StepIO {
     int check_step = 0;
     float* p_out = nullptr;
     bool density_only = false;            // stop after the density update (WaveStepper API)
+    // pair-loop phase shift (USTFWI_PAIR_LAG): the leader records lag_rec[k] after its k-th
+    // pass of the step, the follower waits for lag_wait[k] before its k-th pass
+    cudaEvent_t* lag_rec = nullptr;
+    cudaEvent_t* lag_wait = nullptr;
     cudaEvent_t wait_before_z = nullptr;  // cross-stream dependency of the pressure kernel
     // absorbing media
     float abs_sign = 1.f;                 // absorption_sign (-1 in the time-reversal replay)
@@ -476,14 +482,25 @@ bool chain_enabled(const Ctx& c) {
 // kz-column slabs through the three passes with the slab's spectra resident in L2
 // (launch_chain, USTFWI_CHAIN).
 void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
-    const GridDev& g = c.g;
+    GridDev g = c.g;
+    g.pgrid = s.pgrid;
+    int pass_k = 0;
+    auto before = [&]() {
+        if (io.lag_wait) CK(cudaStreamWaitEvent(st, io.lag_wait[pass_k], 0));
+    };
+    auto after = [&]() {
+        if (io.lag_rec) CK(cudaEventRecord(io.lag_rec[pass_k], st));
+        ++pass_k;
+    };
     const double SB = static_cast<double>(g.rows) * g.nzh * sizeof(float2);  // one half spectrum
     const double FB = static_cast<double>(g.N) * sizeof(float);               // one real field
     auto pencil = [&](int axis, bool inv, const PencilJobs& j) {
         int loads = 0;
         for (int q = 0; q < j.n; ++q)
             if (q == 0 || j.job[q].src != j.job[q - 1].src) ++loads;
+        before();
         c.launch(axis == 0 ? KIND_X : KIND_Y, (loads + j.n) * SB, [&] { return launch_pencil(axis, inv, g, j, st); }, st);
+        after();
     };
     // one y-x-y chain: fused when supported, else three launches
     auto chain = [&](const PencilJobs& ya, const PencilJobs& xb, const PencilJobs& yc) {
@@ -518,8 +535,10 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     // Z: c2r (D_z+ on S2), velocity update, r2c of v
     Pml ps{{stag[0], stag[1], stag[2]}};
     const double coef_b = c.dtr_stag[0].field ? 3 * FB : 0.0;
+    before();
     c.launch(KIND_ZVEL, 6 * SB + 6 * FB + coef_b,
              [&] { return launch_zvel(g, s.S, c.dmul[2][ST_PLUS], s.v, ps, c.dtr_stag, st); }, st);
+    after();
     // chain 2: Fy of Fz v_a; X: kappa D_x-, kappa, kappa; Y^-1 (D_y- on S1)
     ya.n = 3;
     for (int f = 0; f < 3; ++f) ya.job[f] = {f, f, nullptr, 0};
@@ -568,7 +587,9 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     const bool split = !use_generic_kernels() && fast_rows_supported(g.nz);
     const double zb = 4 * SB + (split ? 11 : 8) * FB + (c.dtrho0.field ? FB : 0.0) + (io.corr.grad ? 5 * FB : 0.0);
     if (io.wait_before_z) CK(cudaStreamWaitEvent(st, io.wait_before_z, 0));
+    before();
     c.launch(KIND_ZRHO, zb, [&] { return launch_zrho(g, a, true, st); }, st);
+    after();
     if (split) ++c.launches;
     if (c.absorbing && !io.density_only) absorbing_tail(c, s, io, st);
 }
@@ -1000,8 +1021,29 @@ void gradient_core(Ctx& c, int thickness, bool accumulate) {
     run_step(c, rep, rio, sb);
     acc_push(c, rep, 1, sb);
 
+    // experiments (off by default): USTFWI_PAIR_GRID=k runs the pair loop's pencil passes on
+    // persistent grids of k CTAs per SM; USTFWI_PAIR_LAG=1 makes the replay's k-th pass of a
+    // step wait for the adjoint's k-th pass, so an x pass of one stream meets a y pass of the
+    // other (complementary: issue bound vs HBM bound)
+    static const int pair_grid = [] {
+        const char* e = std::getenv("USTFWI_PAIR_GRID");
+        return e ? std::atoi(e) : 0;
+    }();
+    static const int pair_lag = [] {
+        const char* e = std::getenv("USTFWI_PAIR_LAG");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (dual && pair_grid > 0) {
+        int nsm = 0;
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
+        adj.pgrid = rep.pgrid = pair_grid * nsm;
+    }
     StepIO aio;
     aio.inj = c.adj.view(c.q);
+    if (dual && pair_lag) {
+        aio.lag_rec = c.ev_lag;
+        rio.lag_wait = c.ev_lag;
+    }
     const float inv_dt = static_cast<float>(1.0 / c.grid.dt);
     for (int n = 1; n <= last - 1; ++n) {
         aio.step_n = n;
@@ -1030,6 +1072,7 @@ void gradient_core(Ctx& c, int thickness, bool accumulate) {
         CK(cudaEventRecord(c.ev_join, sb));
         CK(cudaStreamWaitEvent(sa, c.ev_join, 0));
     }
+    adj.pgrid = rep.pgrid = 0;
 }
 
 bool use_graphs() {
@@ -1216,6 +1259,7 @@ int ustfwi_gpu_create(int device, const ustfwi_grid* grid, ustfwi_gpu_ctx** out)
             CK(cudaEventCreateWithFlags(&c->ev_rep[k], cudaEventDisableTiming));
         }
         CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        for (auto& e : c->ev_lag) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         c->grid = *grid;
         c->ndim = grid->ndim;
@@ -1348,6 +1392,8 @@ void ustfwi_gpu_destroy(ustfwi_gpu_ctx* c) {
     }
     for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : {c->ev_adj[0], c->ev_adj[1], c->ev_rep[0], c->ev_rep[1], c->ev_fork, c->ev_join})
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_lag)
         if (e) cudaEventDestroy(e);
     for (void* p : c->allocs) cudaFree(p);
     if (c->stream2) {

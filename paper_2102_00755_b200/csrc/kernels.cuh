@@ -26,6 +26,7 @@ struct GridDev {
     float half_cdt;             // 0.5 * c_ref * dt   (kappa = sinc(half_cdt*|k|), engine.hpp:43)
     float inv_n;                // 1/N (RealFft::inverse normalisation, fft.hpp:58-63)
     int x0, xn;                 // x-plane window of the y and z passes (chunked steps): [x0, x0+xn)
+    int pgrid;                  // persistent pencil grid override (0: MINB CTAs per SM)
 };
 
 // Sparse mass-source injection: unique sorted flat positions, CSR into contributions.

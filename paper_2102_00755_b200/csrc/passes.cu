@@ -1396,7 +1396,8 @@ cudaError_t run_pencil(const GridDev& g, const PencilJobs& j, cudaStream_t st) {
     constexpr size_t smem = AXIS == 0 ? C::SMEM_X : C::SMEM;
     once_per_device(configured, [&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
     const int ntiles = ((g.nzh + TB - 1) / TB) * (AXIS == 0 ? g.ny : g.xn);
-    const int grid = (!DB || ntiles < sm_count() * MINB) ? ntiles : sm_count() * MINB;
+    int grid = (!DB || ntiles < sm_count() * MINB) ? ntiles : sm_count() * MINB;
+    if (DB && g.pgrid > 0 && g.pgrid < grid) grid = g.pgrid;
     kern<<<grid, C::NT, smem, st>>>(g, j);
     return cudaGetLastError();
 }
@@ -1472,7 +1473,8 @@ cudaError_t run_pencil_tma(const GridDev& g, const PencilJobs& j, cudaStream_t s
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     });
     const int ntiles = ((g.nzh + TB - 1) / TB) * (AXIS == 0 ? g.ny : g.xn);
-    const int grid = (!DB || ntiles < sm_count() * MINB) ? ntiles : sm_count() * MINB;
+    int grid = (!DB || ntiles < sm_count() * MINB) ? ntiles : sm_count() * MINB;
+    if (DB && g.pgrid > 0 && g.pgrid < grid) grid = g.pgrid;
     static int occ = -1;
     if (occ < 0) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::NT, smem);
