@@ -463,13 +463,16 @@ void absorbing_tail(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
 // B200 at config D it measured 1.49 ms per chain launch against 0.50 + 0.89 ms for the three
 // separate launches of the two chains (ncu: L2 hit rate 34 %, 2.9 GB of DRAM traffic for
 // chain 1 against a 0.95 GB model: two live 44 MB slabs do not stay resident)
-bool chain_enabled(const Ctx& c) {
-    static int on = -1;
-    if (on < 0) {
+int chain_mode() {
+    static int m = -1;
+    if (m < 0) {
         const char* e = std::getenv("USTFWI_CHAIN");
-        on = (e && e[0] == '1') ? 1 : 0;
+        m = e ? std::atoi(e) : 0;
     }
-    return on == 1 && !use_generic_kernels() && chain_supported(c.g) && c.sim[0].chain_ctr;
+    return m;
+}
+bool chain_enabled(const Ctx& c) {
+    return chain_mode() > 0 && !use_generic_kernels() && chain_supported(c.g) && c.sim[0].chain_ctr;
 }
 
 // One leapfrog step of a stepper: update_velocity_density (engine.hpp:270-292), sparse
@@ -503,8 +506,8 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
         after();
     };
     // one y-x-y chain: fused when supported, else three launches
-    auto chain = [&](const PencilJobs& ya, const PencilJobs& xb, const PencilJobs& yc) {
-        if (chain_enabled(c)) {
+    auto chain = [&](const PencilJobs& ya, const PencilJobs& xb, const PencilJobs& yc, bool fuse) {
+        if (fuse && chain_enabled(c)) {
             // algorithmic bytes of the fused chain: the first reads and the last writes only
             int la = 0;
             for (int q = 0; q < ya.n; ++q)
@@ -531,7 +534,8 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     yc.job[0] = {0, 0, nullptr, 0};
     yc.job[1] = {1, 2, nullptr, 0};
     yc.job[2] = {1, 1, c.dmul[1][ST_PLUS], 0};
-    chain(ya, xb, yc);
+    // chain 1 fused only in mode 1 (its slab holds up to three fields)
+    chain(ya, xb, yc, chain_mode() == 1);
     // Z: c2r (D_z+ on S2), velocity update, r2c of v
     Pml ps{{stag[0], stag[1], stag[2]}};
     const double coef_b = c.dtr_stag[0].field ? 3 * FB : 0.0;
@@ -550,7 +554,20 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     yc.job[0] = {0, 0, nullptr, 0};
     yc.job[1] = {1, 1, c.dmul[1][ST_MINUS], 0};
     yc.job[2] = {2, 2, nullptr, 0};
-    chain(ya, xb, yc);
+    if (chain_enabled(c) && chain_mode() == 2) {
+        // the three fields of chain 2 are independent through all three passes: one fused
+        // single-field chain each keeps one 14.7 MB slab per field live in L2
+        for (int f = 0; f < 3; ++f) {
+            PencilJobs a1 = ya, b1 = xb, c1 = yc;
+            a1.n = b1.n = c1.n = 1;
+            a1.job[0] = ya.job[f];
+            b1.job[0] = xb.job[f];
+            c1.job[0] = yc.job[f];
+            chain(a1, b1, c1, true);
+        }
+    } else {
+        chain(ya, xb, yc, true);
+    }
     // Z: c2r (D_z- on S2), density update, sparse ops, pressure, gathers, Fz p -> S0
     ZrhoArgs a{};
     for (int f = 0; f < 3; ++f) {
