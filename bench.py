@@ -429,7 +429,7 @@ def b200_arm(a):
                    "share_of_profiled_gradient": v[0] / prof_ms if prof_ms else 0.0} for k, v in stats.items() if v[1]}
     n = g.points
     b_model = n * (BYTES_PER_VU_MODEL * (3 * g.nt - 3) + BYTES_CORR_MODEL * (g.nt - 2))
-    path_gbps = b_model / s_per_step / 1e9
+    path_gbps = b_model * slots / s_per_step / 1e9   # gradients per GPU per step = slots
     # the engine's own algorithmic bytes per voxel-update (sum over launch classes) and the
     # ncu-measured DRAM bytes of the same launches where a launch list is committed
     alg_bytes = sum(v[2] for v in stats.values())

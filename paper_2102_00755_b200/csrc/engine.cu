@@ -65,6 +65,10 @@ struct StepperState {
 struct InjectSet {
     int n_unique = 0;
     std::vector<int> h_pos;            // unique positions
+    std::vector<size_t> h_order;       // contribution order of the CSR arrays (stable sort by position)
+    std::vector<size_t> h_src_pos;     // the positions / offsets / lengths the set was built from
+    std::vector<int> h_off, h_len;
+    size_t h_total = 0;
     int* pos = nullptr;
     int* csr = nullptr;
     int* off = nullptr;
@@ -637,6 +641,7 @@ void build_inject(Ctx& c, InjectSet& set, const std::vector<size_t>& pos, const 
     std::vector<size_t> order(n);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return pos[a] < pos[b]; });
+    set.h_order = order;
     std::vector<int> upos, csr{0}, o, l, st, d;
     std::vector<float> ww;
     for (size_t k = 0; k < n; ++k) {
@@ -1568,7 +1573,6 @@ int ustfwi_gpu_set_gradient_param(ustfwi_gpu_ctx* c, int param) {
 int ustfwi_gpu_set_sources(ustfwi_gpu_ctx* c, size_t n_src, const size_t* pos, const size_t* sig_off,
                            const double* sig, const double* weights, const int32_t* delay_steps) {
     return guarded(c, [&] {
-        c->touch();
         const size_t N = static_cast<size_t>(c->g.N);
         std::vector<size_t> p(pos, pos + n_src);
         for (size_t v : p)
@@ -1583,9 +1587,31 @@ int ustfwi_gpu_set_sources(ustfwi_gpu_ctx* c, size_t n_src, const size_t* pos, c
             if (weights) w[i] = static_cast<float>(weights[i]);
             if (delay_steps) delay[i] = delay_steps[i];
         }
-        c->release(c->src.sig);
-        c->src.sig = c->upload(to_f32(sig, total));
-        build_inject(*c, c->src, p, off, len, stride, delay, w);
+        InjectSet& set = c->src;
+        if (set.sig && n_src > 0 && p == set.h_src_pos && off == set.h_off && len == set.h_len && total == set.h_total) {
+            // same emitters, new realization (weights / delays / signal values): update the
+            // existing device tables in place, so a captured gradient graph stays valid
+            std::vector<int> d(n_src);
+            std::vector<float> ww(n_src);
+            for (size_t k = 0; k < n_src; ++k) {
+                d[k] = delay[set.h_order[k]];
+                ww[k] = w[set.h_order[k]];
+            }
+            const auto sf = to_f32(sig, total);
+            CK(cudaMemcpyAsync(set.delay, d.data(), n_src * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(set.w, ww.data(), n_src * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(set.sig, sf.data(), total * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            return;
+        }
+        c->touch();
+        c->release(set.sig);
+        set.sig = c->upload(to_f32(sig, total));
+        build_inject(*c, set, p, off, len, stride, delay, w);
+        set.h_src_pos = p;
+        set.h_off = off;
+        set.h_len = len;
+        set.h_total = total;
         c->src_pos_host = p;
         CK(cudaStreamSynchronize(c->stream));
     });
