@@ -77,7 +77,8 @@ def main():
             eng.set_sensors(sc.sensors)
             obs, _ = eng.forward(0)
             eng.set_medium(sc.model)
-            eng.gradient_tr(obs, sc.thickness)  # warm-up
+            eng.gradient_tr(obs, sc.thickness)  # warm-up: eager launches
+            eng.gradient_tr(obs, sc.thickness)  # warm-up: CUDA-graph capture
             t0 = time.perf_counter()
             eng.gradient_tr(obs, sc.thickness)
             dt = time.perf_counter() - t0
