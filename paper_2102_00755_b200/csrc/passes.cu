@@ -1377,6 +1377,219 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR, USTFWI_ZP_MINB) zp2_kerne
 // ======================================================================================
 namespace {
 
+// Density update of all three axes and the pressure step in one CTA per row block
+// (engine.hpp:284-291 + :296-347): per axis the staged spectrum rows are inverse transformed
+// (D_z- on z), rho_a = pml_a (pml_a rho_a - dt rho0 dv_a) is formed in registers, the sparse
+// work of the owner thread (sources += amp * scale, shell = value, reference order) is applied
+// to the register value, rho_a is stored and summed; then p = c0^2 sum_a rho_a, the TR
+// correlation, the gathers and the r2c of p follow as in zp2_kernel. Against the split
+// zrho2_axis + zp2 pair it does not re-read the three split densities (48 instead of 60 B per
+// voxel). Non-absorbing steps only (the absorbing path keeps the raw derivatives).
+#ifndef USTFWI_PASSES_Y_ONLY
+template <int M, int N1, int RW>
+__global__ void __launch_bounds__(RW * Z2<M, N1>::TPR, 4) zrhop_kernel(const __grid_constant__ ZrhoFastArgs P) {
+    using C = Z2<M, N1>;
+    constexpr int N2 = C::N2, TPR = C::TPR, NA = C::NA, NZ = C::NZ, VP = C::VP, NT = RW * TPR;
+    extern __shared__ __align__(128) unsigned char sm_raw[];
+    const GridDev& g = P.g;
+    const ZrhoArgs& A = P.a;
+    const bool coef_field = A.dtrho0.field != nullptr;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm_raw);   // [0] spectra + rho rows, [1] coefficient rows
+    __shared__ int sp[8];
+    float2* twB = reinterpret_cast<float2*>(sm_raw + 32);  // c2r twiddles
+    float2* twA = twB + M;                                   // r2c twiddles
+    float2* sS = twA + M;                                    // [RW][nzp] staged spectrum rows
+    float2* zt = sS;                                         // aliases sS (z2_c2r_b)
+    float* sR = reinterpret_cast<float*>(zt + RW * cmax(g.nzp, C::ZT));  // rho_a rows
+    float* sSum = sR + RW * VP;                              // running sum_a rho_a (owner-private slots)
+    float* sD = sSum + RW * VP;                              // dt*rho0 rows (optional)
+    const long long row0 = (long long)g.x0 * g.ny + (long long)blockIdx.x * RW;
+    const int nrows = (int)min((long long)RW, (long long)(g.x0 + g.xn) * g.ny - row0);
+    const long long i0 = row0 * NZ;
+    const int lo_key = (int)i0;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+    }
+    if (threadIdx.x < 4) {  // one sparse set per thread
+        const int k = threadIdx.x;
+        if (k == 0) sparse_range(A.inj.pos, A.inj.n_unique, A.inj.blk8, row0, nrows, NZ, sp[0], sp[1]);
+        if (k == 1) sparse_range(A.enf.pos, A.enf.n, A.enf.blk8, row0, nrows, NZ, sp[2], sp[3]);
+        if (k == 2) sparse_range(A.sens.pos, A.sens.n, A.sens.blk8, row0, nrows, NZ, sp[4], sp[5]);
+        if (k == 3) sparse_range(A.shell.pos, A.shell.n, A.shell.blk8, row0, nrows, NZ, sp[6], sp[7]);
+    }
+    for (int i = threadIdx.x; i < M; i += NT) {
+        twB[i] = g.pzh.tw[(i / N1) * (i % N1)];
+        twA[i] = g.pzh.tw[(i / N2) * (i % N2)];
+    }
+    __syncthreads();  // barriers initialised
+    auto stage = [&](int a) {  // thread 0 arms, warp 0 issues the axis's bulk copies
+        if (threadIdx.x == 0)
+            mbar_arrive_expect_tx(&bar[0], nrows * g.nzp * 8u + nrows * NZ * 4u);
+        __syncwarp();
+        if (threadIdx.x < 32) {
+            const int l = threadIdx.x;
+            if (l == 0) bulk_g2s(sS, A.S[a] + row0 * g.nzp, nrows * g.nzp * 8u, &bar[0]);
+            for (int i = l; i < nrows; i += 32) bulk_g2s(sR + i * VP, A.rho[a] + (row0 + i) * NZ, NZ * 4u, &bar[0]);
+        }
+    };
+    if (coef_field && threadIdx.x < 32) {
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(&bar[1], nrows * NZ * 4u);
+        __syncwarp();
+        for (int i = threadIdx.x; i < nrows; i += 32)
+            bulk_g2s(sD + i * VP, A.dtrho0.field + (row0 + i) * NZ, NZ * 4u, &bar[1]);
+    }
+    const int a_first = max(A.a_first, 0);
+    stage(a_first);
+    int r, t;
+    z2_thread<TPR>(threadIdx.x, r, t);
+    const bool rowok = r < nrows;
+    const long long row = row0 + r;
+    const int x = rowok ? (int)(row / g.ny) : 0, y = rowok ? (int)(row % g.ny) : 0;
+    const float2 wr0 = g.tw_rfft[t], wr1 = g.tw_rfft[t == 0 ? N1 / 2 : N1 - t];
+    float2* ztr = zt + r * C::ZT;
+    // owner of flat position pos: row, pair n = z/2 with n % N2 in this thread's codelets
+    auto owns = [&](int pos, int& j, int& n1, int& comp) {
+        const int tt = pos - lo_key;
+        const int rr = tt / NZ, z = tt % NZ, n = z >> 1;
+        comp = z & 1;
+        const int n2 = n % N2;
+        if (!(rowok && rr == r && n2 % TPR == t)) return false;
+        j = n2 / TPR;
+        n1 = n / N2;
+        return true;
+    };
+    float* sumr = sSum + r * VP;
+    if (coef_field) mbar_wait(&bar[1], 0);
+    const float dsc = A.dtrho0.scalar;
+
+    unsigned phase = 0;
+    for (int a = a_first; a < 3; ++a) {
+        mbar_wait(&bar[0], phase);
+        phase ^= 1u;
+        z2_c2r_b<M, N1>(sS + r * g.nzp, a == 2 ? A.dz_minus : nullptr, twB, wr0, wr1, t, ztr, rowok);
+        __syncthreads();
+        float2 q[NA][N1];
+        if (rowok) {
+            const float pa = a == 0 ? __ldg(A.pml.prof[0] + x) : (a == 1 ? __ldg(A.pml.prof[1] + y) : 0.f);
+            const float* rs = sR + r * VP;
+            const float* ds = sD + r * VP;
+#pragma unroll
+            for (int j = 0; j < NA; ++j) {
+                const int n2 = t + TPR * j;
+                float2 u[N1];
+                z2_c2r_a<M, N1>(ztr, n2, g.inv_n, u);
+#pragma unroll
+                for (int n1 = 0; n1 < N1; ++n1) {
+                    const int n = n2 + N2 * n1;
+                    float2 v = *reinterpret_cast<const float2*>(rs + 2 * n);
+                    float2 pm = make_float2(pa, pa);
+                    if (a == 2) pm = __ldg(reinterpret_cast<const float2*>(A.pml.prof[2]) + n);
+                    float2 d = make_float2(dsc, dsc);
+                    if (coef_field) d = *reinterpret_cast<const float2*>(ds + 2 * n);
+                    v.x = pm.x * (pm.x * v.x - d.x * u[n1].x);
+                    v.y = pm.y * (pm.y * v.y - d.y * u[n1].y);
+                    q[j][n1] = v;
+                }
+            }
+            // sparse density updates of the owner thread, in the reference order (sources,
+            // then the shell), on the register values
+            auto modify = [&](int pos, bool set, float val) {
+                int j, n1, comp;
+                if (!owns(pos, j, n1, comp)) return;
+#pragma unroll
+                for (int jj = 0; jj < NA; ++jj)
+#pragma unroll
+                    for (int k = 0; k < N1; ++k)
+                        if (jj == j && k == n1) {
+                            float& e = comp ? q[jj][k].y : q[jj][k].x;
+                            e = set ? val : e + val;
+                        }
+            };
+            for (int uu = sp[0]; uu < sp[1]; ++uu) {
+                const int pos = A.inj.pos[uu];
+                const float sc = A.inj.scale[uu];
+                for (int cc = A.inj.csr[uu]; cc < A.inj.csr[uu + 1]; ++cc) {
+                    const int n = A.step_n - A.inj.delay[cc];
+                    if (n < 0 || n >= A.inj.len[cc]) continue;
+                    const float amp = A.inj.w[cc] * A.inj.sig[A.inj.off[cc] + (long long)n * A.inj.stride[cc]];
+                    if (amp == 0.f) continue;
+                    modify(pos, false, amp * sc);
+                }
+            }
+            for (int qq = sp[2]; qq < sp[3]; ++qq) {
+                const int pos = A.enf.pos[qq];
+                modify(pos, true, A.enf.vals[qq] / (A.enf.ndim * A.c0sq[pos]));
+            }
+#pragma unroll
+            for (int j = 0; j < NA; ++j) {
+                const int n2 = t + TPR * j;
+#pragma unroll
+                for (int n1 = 0; n1 < N1; ++n1) {
+                    const int n = n2 + N2 * n1;
+                    *reinterpret_cast<float2*>(A.rho[a] + row * NZ + 2 * n) = q[j][n1];
+                    float2* sm2 = reinterpret_cast<float2*>(sumr + 2 * n);
+                    if (a == a_first) {
+                        *sm2 = q[j][n1];
+                    } else {
+                        const float2 o = *sm2;
+                        *sm2 = make_float2(o.x + q[j][n1].x, o.y + q[j][n1].y);
+                    }
+                }
+            }
+        }
+        __syncthreads();  // sS / sR free for the next axis
+        if (a + 1 < 3) stage(a + 1);
+    }
+
+    float2 pv[NA][N1];
+    if (rowok) {
+#pragma unroll
+        for (int j = 0; j < NA; ++j) {
+            const int n2 = t + TPR * j;
+#pragma unroll
+            for (int n1 = 0; n1 < N1; ++n1) {
+                const long long i = row * NZ + 2 * (n2 + N2 * n1);
+                const float2 c2 = __ldg(reinterpret_cast<const float2*>(A.c0sq + i));
+                const float2 sm = *reinterpret_cast<const float2*>(sumr + 2 * (n2 + N2 * n1));
+                float2 p;
+                p.x = c2.x * sm.x;
+                p.y = c2.y * sm.y;
+                *reinterpret_cast<float2*>(A.p_out + i) = p;
+                pv[j][n1] = p;
+                if (A.corr.grad != nullptr) {
+                    const float2 pm = *reinterpret_cast<const float2*>(A.corr.p_mid + i);
+                    const float2 po = *reinterpret_cast<const float2*>(A.corr.p_old + i);
+                    const float2 qa = *reinterpret_cast<const float2*>(A.corr.q_adj + i);
+                    float2 gv = *reinterpret_cast<const float2*>(A.corr.grad + i);
+                    const float wx = 2.f / (c2.x * sqrtf(c2.x)), wy = 2.f / (c2.y * sqrtf(c2.y));
+                    gv.x += wx * (((p.x - 2.f * pm.x) + po.x) * A.corr.inv_dt) * qa.x;
+                    gv.y += wy * (((p.y - 2.f * pm.y) + po.y) * A.corr.inv_dt) * qa.y;
+                    *reinterpret_cast<float2*>(A.corr.grad + i) = gv;
+                }
+            }
+        }
+        if (A.check_step > 0 && row == 0 && t == 0 && !isfinite(pv[0][0].x)) atomicMin(A.diverged, A.check_step);
+        auto gather = [&](int pos, float* out) {
+            int j, n1, comp;
+            if (!owns(pos, j, n1, comp)) return;
+#pragma unroll
+            for (int jj = 0; jj < NA; ++jj)
+#pragma unroll
+                for (int k = 0; k < N1; ++k)
+                    if (jj == j && k == n1) *out = comp ? pv[jj][k].y : pv[jj][k].x;
+        };
+        for (int s2 = sp[4]; s2 < sp[5]; ++s2) gather(A.sens.pos[s2], A.sens.out + A.sens.idx[s2]);
+        for (int q2 = sp[6]; q2 < sp[7]; ++q2) gather(A.shell.pos[q2], A.shell.out + q2);
+#pragma unroll
+        for (int j = 0; j < NA; ++j) z2_r2c_a<M, N1>(pv[j], t + TPR * j, twA, ztr);
+    }
+    __syncthreads();
+    if (rowok) z2_r2c_b<M, N1>(ztr, wr0, wr1, t, A.S[0] + row * g.nzp);
+}
+#endif  // !USTFWI_PASSES_Y_ONLY
+
 int sm_count() {
     static int n = 0;
     if (n == 0) {
@@ -2069,8 +2282,29 @@ cudaError_t zvel2_run(const GridDev& g, const ZvelFastArgs& a, cudaStream_t st) 
     kern<<<blocks, RW * Z2<M, N1>::TPR, smem, st>>>(a);
     return cudaGetLastError();
 }
+// USTFWI_ZFUSE=1: the density update of the three axes and the pressure step in one kernel
+// (zrhop_kernel) instead of zrho2_axis + zp2 (non-absorbing steps)
+bool use_zfuse() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = std::getenv("USTFWI_ZFUSE");
+        on = (e && e[0] == '1') ? 1 : 0;
+    }
+    return on == 1;
+}
+
 template <int M, int N1, int RW>
 cudaError_t zrho2_run(const GridDev& g, const ZrhoFastArgs& a, cudaStream_t st) {
+    if (use_zfuse() && !a.a.du_out[0] && !a.a.du_out[1] && !a.a.du_out[2]) {
+        using C = Z2<M, N1>;
+        const size_t smem = 32 + size_t(2 * M) * 8 + size_t(RW) * cmax(g.nzp, C::ZT) * 8 +
+                            size_t(a.a.dtrho0.field ? 3 : 2) * RW * C::VP * 4;
+        auto kf = zrhop_kernel<M, N1, RW>;
+        cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const unsigned blocks = (unsigned)(((long long)g.xn * g.ny + RW - 1) / RW);
+        kf<<<blocks, RW * C::TPR, smem, st>>>(a);
+        return cudaGetLastError();
+    }
     const size_t smem = Z2Smem<M, N1, RW>::bytes_rho(g.nzp, a.a.dtrho0.field ? 2 : 1);
     auto kern = zrho2_axis_kernel<M, N1, RW>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

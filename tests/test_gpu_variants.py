@@ -61,6 +61,7 @@ def run(env_extra, layout):
     ("y", {"USTFWI_PENCIL_TMA": "0"}), ("y", {"USTFWI_ZROW2": "0"}), ("y", {"USTFWI_GENERIC": "1"}),
     ("x", {"USTFWI_X480": "1"}), ("x", {"USTFWI_PENCIL_TMA": "0"}),
     ("xy", {"USTFWI_CHAIN": "1"}), ("xy", {"USTFWI_GRAPH": "0"}),
+    ("y", {"USTFWI_ZFUSE": "1"}), ("x", {"USTFWI_ZFUSE": "1"}),
 ])
 def test_kernel_variants_agree(layout, variant):
     base = run({}, layout)
