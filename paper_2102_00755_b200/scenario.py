@@ -248,5 +248,33 @@ def encoding_problem(n_src: int, nt: Optional[int] = None):
     return g, model, truth, srcs, sens, pulse
 
 
+def config_d_gradient_problem():
+    """The config-D grid and phantom with 16 emitters and 16 receivers on rings 6 voxels outside
+    Gamma (z = 40 and 60) and the config-D pulse advanced by 150 samples (peak near sample 52),
+    so that a 100-step gradient already sees the wavefield cross the shell: the full-size parity
+    case of the TR gradient (tests/golden/make_golden_large.py Dgrad, tests/test_gpu_large.py).
+    Returns (scenario with nt = 100, emitters, receivers, pulse)."""
+    sc = config_d(nt=100)
+    sh = sc.grid.shape
+    gam = np.asarray(sc.model.gamma, bool)
+    cx = cy = sh[0] // 2
+    full = config_d().pulse          # the untruncated pulse of the config-D grid
+    pulse = np.asarray(full[150:250], np.float64)
+
+    def ring(z, off):
+        r_g = 0
+        while gam[cx + r_g + 1, cy, z]:
+            r_g += 1
+        rr = r_g + 6
+        pts = []
+        for k in range(16):
+            th = 2 * np.pi * (k + off) / 16
+            x, y = int(round(cx + rr * np.cos(th))), int(round(cy + rr * np.sin(th)))
+            assert not gam[x, y, z]
+            pts.append(flat(sh, x, y, z))
+        return pts
+    return sc, ring(40, 0.0), ring(60, 0.5), pulse
+
+
 CONFIGS = {"A": config_a, "B": config_b, "C": config_c, "D": config_d,
            "E0": lambda nt=None: config_e(0, nt), "E1": lambda nt=None: config_e(1, nt)}

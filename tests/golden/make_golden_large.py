@@ -7,6 +7,7 @@ Run here (where /root/reference exists), one fixture per process (hours of fp64 
     python tests/golden/make_golden_large.py D       # config D grid + bench phantom + 1024 encoded emitters, nt = 160
     python tests/golden/make_golden_large.py drift   # config A geometry at nt = 3912 (fp32 drift over 3*3912 steps)
     python tests/golden/make_golden_large.py rho0    # config A (nt = 393), heterogeneous rho0: rho0 and c0 gradients
+    python tests/golden/make_golden_large.py Dgrad   # config-D grid, 16 + 16 transducers next to Gamma, nt = 100 TR gradient
 
 Every input is built exactly as bench.py / scenario.py build it (same seeds, same encoding
 realization r = 0 of master seed 20210201, tau = 0), so the device run in
@@ -100,6 +101,53 @@ def config_d_fixture(nt=160):
     print(f"config_d_short: forward {t1 - t0:.0f}s, |data| {np.linalg.norm(data):.6e}", flush=True)
 
 
+def config_d_gradient_problem():
+    """The config-D grid and phantom with 16 emitters and 16 receivers on rings 6 voxels outside
+    Gamma (z = 40 and 60) and a pulse advanced by 150 samples (peak near sample 52), so that a
+    100-step gradient already sees the wavefield cross the shell: the 480-point pencils, the
+    nz = 256 rows, the 1.16 M-voxel shell record / replay and the correlation at full size.
+    Shared with tests/test_gpu_large.py."""
+    sc = scenario.config_d(nt=100)
+    sh = sc.grid.shape
+    gam = np.asarray(sc.model.gamma, bool)
+    cx = cy = sh[0] // 2
+    full = scenario.config_d().pulse          # the untruncated pulse of the config-D grid
+    pulse = np.asarray(full[150:250], np.float64)
+
+    def ring(z, off):
+        r_g = 0
+        while gam[cx + r_g + 1, cy, z]:
+            r_g += 1
+        rr = r_g + 6
+        pts = []
+        for k in range(16):
+            th = 2 * np.pi * (k + off) / 16
+            x, y = int(round(cx + rr * np.cos(th))), int(round(cy + rr * np.sin(th)))
+            assert not gam[x, y, z]
+            pts.append(scenario.flat(sh, x, y, z))
+        return pts
+    return sc, ring(40, 0.0), ring(60, 0.5), pulse
+
+
+def config_d_gradient_fixture():
+    sc, emit, recv, pulse = config_d_gradient_problem()
+    g = sc.grid
+    sig = [pulse * (1.0 if k % 2 == 0 else -1.0) for k in range(len(emit))]  # a fixed +-1 encoding
+    observed = np.zeros((len(recv), g.nt))
+    t0 = time.time()
+    loss, grad = ref.gradient_time_reversal(g, sc.model, emit, sig, recv, observed, sc.thickness)
+    t1 = time.time()
+    gidx = np.flatnonzero(np.asarray(sc.model.gamma).ravel())
+    gg = grad.ravel()[gidx]
+    sel = np.flatnonzero(np.abs(gg) > 1e-3 * np.abs(gg).max())
+    np.savez_compressed(os.path.join(OUT, "config_d_grad.npz"), nt=g.nt, loss=loss, grad_norm=np.linalg.norm(gg),
+                        grad_sum=gg.sum(), grad_abs_sum=np.abs(gg).sum(), gamma_count=gidx.size,
+                        grad_sel_idx=gidx[sel], grad_sel=gg[sel].astype(np.float32),
+                        grad_sub_idx=gidx[::211], grad_sub=gg[::211].astype(np.float32),
+                        grad_outside_max=np.abs(np.delete(grad.ravel(), gidx)).max(), seconds=np.array([t1 - t0]))
+    print(f"config_d_grad: {t1 - t0:.0f}s loss {loss:.6e} |g| {np.linalg.norm(gg):.3e} nonzero-ish {sel.size}", flush=True)
+
+
 def rho0_fixture():
     """Heterogeneous rho0 at config A: the rho0 gradient (GradientParam::rho0,
     gradient.hpp:117-128,213-239; oracle/_ref is built with the F3 compile fix) and the c0
@@ -131,4 +179,5 @@ if __name__ == "__main__":
     if not ref.available():
         sys.exit("oracle/_ref missing: make -C oracle")
     which = sys.argv[1] if len(sys.argv) > 1 else ""
-    {"B": config_b_fixture, "D": config_d_fixture, "drift": drift_fixture, "rho0": rho0_fixture}[which]()
+    {"B": config_b_fixture, "D": config_d_fixture, "drift": drift_fixture, "rho0": rho0_fixture,
+     "Dgrad": config_d_gradient_fixture}[which]()

@@ -8,7 +8,9 @@ produced (oracle/_ref, tests/golden/make_golden_large.py; hours of fp64 CPU work
       1024 receivers — the 480-point pencils, the nz = 256 rows, the 1.16 M-voxel shell: traces,
       per-step shell-trace |sums|, the shell-trace subsample on the field's scale;
   fp32 drift, config A geometry at nt = 3912 (the config-D step count): traces and TR gradient
-      after 3 * 3912 - 3 steps.
+      after 3 * 3912 - 3 steps;
+  the TR gradient on the config-D grid (scenario.config_d_gradient_problem: the bench phantom,
+      16 + 16 transducers next to Gamma so that 100 steps already cross the 1.16 M-voxel shell).
 
 Bars (BASELINE.json north_star): traces rel l2 <= 1e-4, gradient rel l2 <= 1e-3."""
 import numpy as np
@@ -105,3 +107,25 @@ def test_config_d_grid_forward_matches_reference(golden):
     assert r_traces < TRACE_TOL
     assert r_steps_abs < TRACE_TOL
     assert a_sub < TRACE_TOL * 1e-1
+
+
+def test_config_d_grid_gradient_matches_reference(golden):
+    z = load(golden, "config_d_grad")
+    sc, emit, recv, pulse = scenario.config_d_gradient_problem()
+    assert sc.grid.nt == int(z["nt"])
+    from paper_2102_00755_b200.engine import SensorArray, SourceSet
+    sig = [pulse * (1.0 if k % 2 == 0 else -1.0) for k in range(len(emit))]
+    with GpuEngine(sc.grid) as eng:
+        eng.set_medium(sc.model)
+        eng.set_sources(SourceSet(emit, sig))
+        eng.set_sensors(SensorArray(recv))
+        loss, grad = eng.gradient_tr(np.zeros((len(recv), sc.grid.nt)), sc.thickness)
+    g = grad.ravel()
+    r_sel = rel(g[z["grad_sel_idx"]], z["grad_sel"])
+    r_sub = rel(g[z["grad_sub_idx"]], z["grad_sub"])
+    r_norm = abs(np.linalg.norm(g[np.asarray(sc.model.gamma, bool).ravel()]) - float(z["grad_norm"])) / float(z["grad_norm"])
+    r_loss = abs(loss - float(z["loss"])) / float(z["loss"])
+    print(f"config D grid gradient (nt {sc.grid.nt}): loss {r_loss:.2e}, gradient on |g| > 1e-3 max "
+          f"({len(z['grad_sel_idx'])} voxels) {r_sel:.2e}, strided subsample {r_sub:.2e}, norm {r_norm:.2e}")
+    assert r_loss < TRACE_TOL
+    assert r_sel < GRAD_TOL and r_sub < GRAD_TOL and r_norm < GRAD_TOL
