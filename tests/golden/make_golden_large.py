@@ -101,36 +101,8 @@ def config_d_fixture(nt=160):
     print(f"config_d_short: forward {t1 - t0:.0f}s, |data| {np.linalg.norm(data):.6e}", flush=True)
 
 
-def config_d_gradient_problem():
-    """The config-D grid and phantom with 16 emitters and 16 receivers on rings 6 voxels outside
-    Gamma (z = 40 and 60) and a pulse advanced by 150 samples (peak near sample 52), so that a
-    100-step gradient already sees the wavefield cross the shell: the 480-point pencils, the
-    nz = 256 rows, the 1.16 M-voxel shell record / replay and the correlation at full size.
-    Shared with tests/test_gpu_large.py."""
-    sc = scenario.config_d(nt=100)
-    sh = sc.grid.shape
-    gam = np.asarray(sc.model.gamma, bool)
-    cx = cy = sh[0] // 2
-    full = scenario.config_d().pulse          # the untruncated pulse of the config-D grid
-    pulse = np.asarray(full[150:250], np.float64)
-
-    def ring(z, off):
-        r_g = 0
-        while gam[cx + r_g + 1, cy, z]:
-            r_g += 1
-        rr = r_g + 6
-        pts = []
-        for k in range(16):
-            th = 2 * np.pi * (k + off) / 16
-            x, y = int(round(cx + rr * np.cos(th))), int(round(cy + rr * np.sin(th)))
-            assert not gam[x, y, z]
-            pts.append(scenario.flat(sh, x, y, z))
-        return pts
-    return sc, ring(40, 0.0), ring(60, 0.5), pulse
-
-
 def config_d_gradient_fixture():
-    sc, emit, recv, pulse = config_d_gradient_problem()
+    sc, emit, recv, pulse = scenario.config_d_gradient_problem()
     g = sc.grid
     sig = [pulse * (1.0 if k % 2 == 0 else -1.0) for k in range(len(emit))]  # a fixed +-1 encoding
     observed = np.zeros((len(recv), g.nt))
