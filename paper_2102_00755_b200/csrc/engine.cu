@@ -2,6 +2,7 @@
 // engine.hpp:17-386), the forward simulation (simulate.hpp:30-105) and the time-reversal
 // c0 gradient (gradient.hpp:333-464) orchestrated as fused pass launches on one stream,
 // and the device half of the C ABI (include/ustfwi_capi.h).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nvtx3/nvToolsExt.h>
@@ -12,6 +13,7 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -139,6 +141,12 @@ struct ustfwi_gpu_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr;   // time-reversal replay stream of the pair loop
+    // SM-partitioned pair loop (USTFWI_GREEN): adjoint / replay streams of two
+    // green contexts with disjoint SM sets
+    cudaStream_t gstream[2] = {};
+    CUgreenCtx gctx[2] = {};
+    int gsm[2] = {};
+    cudaEvent_t ev_gjoin = nullptr;
     cudaEvent_t ev_adj[2] = {}, ev_rep[2] = {}, ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_lag[8] = {};       // pair-loop phase shift (USTFWI_PAIR_LAG)
     float* adj_p2 = nullptr;          // second adjoint pressure buffer (pair loop)
@@ -407,6 +415,7 @@ struct StepIO {
     // pass of the step, the follower waits for lag_wait[k] before its k-th pass
     cudaEvent_t* lag_rec = nullptr;
     cudaEvent_t* lag_wait = nullptr;
+    int lag_off = 0;                      // ... for the leader's (k + lag_off)-th pass
     cudaEvent_t wait_before_z = nullptr;  // cross-stream dependency of the pressure kernel
     // absorbing media
     float abs_sign = 1.f;                 // absorption_sign (-1 in the time-reversal replay)
@@ -493,7 +502,7 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     g.pgrid = s.pgrid;
     int pass_k = 0;
     auto before = [&]() {
-        if (io.lag_wait) CK(cudaStreamWaitEvent(st, io.lag_wait[pass_k], 0));
+        if (io.lag_wait && pass_k + io.lag_off < 8) CK(cudaStreamWaitEvent(st, io.lag_wait[pass_k + io.lag_off], 0));
     };
     auto after = [&]() {
         if (io.lag_rec) CK(cudaEventRecord(io.lag_rec[pass_k], st));
@@ -979,6 +988,70 @@ void acc_correlate(Ctx& c, Correlate cr, int nw, int mid, int old, cudaStream_t 
     c.count(launch_correlate(c.g.N, c.ring[nw], c.c0sq, cr, st));
 }
 
+// SM partition of the pair loop (USTFWI_GREEN=k, default 54 % of the SMs): the replay stream gets a green
+// context of k SMs (rounded by the driver to its granularity of 8), the adjoint the rest, so
+// the two streams' passes run side by side on disjoint SMs instead of both persistent grids
+// filling the whole device in turn.
+template <class F>
+F driver_fn(const char* name, bool required = true) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || fn == nullptr) {
+        if (required) fail(USTFWI_ERR_CUDA, std::string("driver entry point ") + name + " unavailable");
+        return nullptr;
+    }
+    return reinterpret_cast<F>(fn);
+}
+
+void green_partition(Ctx& c, int want, int prio_a, int prio_b) {
+    auto get_res = driver_fn<CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType)>("cuDeviceGetDevResource");
+    auto split = driver_fn<CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned,
+                                        unsigned)>("cuDevSmResourceSplitByCount");
+    auto gen = driver_fn<CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned)>("cuDevResourceGenerateDesc");
+    auto create = driver_fn<CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned)>("cuGreenCtxCreate");
+    auto mkstream = driver_fn<CUresult (*)(CUstream*, CUgreenCtx, unsigned, int)>("cuGreenCtxStreamCreate");
+    CUdevResource all{}, parts[1]{}, rest{};
+    if (get_res(static_cast<CUdevice>(c.device), &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
+        fail(USTFWI_ERR_CUDA, "cuDeviceGetDevResource failed");
+    unsigned n = 1;
+    if (split(parts, &n, &all, &rest, 0, static_cast<unsigned>(want)) != CUDA_SUCCESS || n != 1)
+        fail(USTFWI_ERR_CUDA, "cuDevSmResourceSplitByCount failed");
+    CUdevResource* res[2] = {&rest, &parts[0]};  // adjoint: the remainder, replay: the k SMs
+    const int prio[2] = {prio_a, prio_b};
+    for (int k = 0; k < 2; ++k) {
+        CUdevResourceDesc d{};
+        if (gen(&d, res[k], 1) != CUDA_SUCCESS) fail(USTFWI_ERR_CUDA, "cuDevResourceGenerateDesc failed");
+        if (create(&c.gctx[k], d, static_cast<CUdevice>(c.device), CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
+            fail(USTFWI_ERR_CUDA, "cuGreenCtxCreate failed");
+        CUstream st{};
+        if (mkstream(&st, c.gctx[k], CU_STREAM_NON_BLOCKING, prio[k]) != CUDA_SUCCESS)
+            fail(USTFWI_ERR_CUDA, "cuGreenCtxStreamCreate failed");
+        c.gstream[k] = reinterpret_cast<cudaStream_t>(st);
+        c.gsm[k] = static_cast<int>(res[k]->sm.smCount);
+    }
+    CK(cudaEventCreateWithFlags(&c.ev_gjoin, cudaEventDisableTiming));
+    if (std::getenv("USTFWI_VERBOSE"))
+        std::fprintf(stderr, "[ustfwi] green partition: adjoint %d SMs, replay %d SMs\n", c.gsm[0], c.gsm[1]);
+}
+
+void drop_green(Ctx& c) {
+    for (int k = 0; k < 2; ++k) {
+        if (c.gstream[k]) {
+            cudaStreamSynchronize(c.gstream[k]);
+            cudaStreamDestroy(c.gstream[k]);
+            c.gstream[k] = nullptr;
+        }
+    }
+    if (c.ev_gjoin) cudaEventDestroy(c.ev_gjoin);
+    c.ev_gjoin = nullptr;
+    static auto destroy = driver_fn<CUresult (*)(CUgreenCtx)>("cuGreenCtxDestroy", false);
+    for (int k = 0; k < 2; ++k) {
+        if (c.gctx[k] && destroy) destroy(c.gctx[k]);
+        c.gctx[k] = nullptr;
+        c.gsm[k] = 0;
+    }
+}
+
 // compute_gradient, TR branch (gradient.hpp:359-462), GradientParam c0 / alpha0 / y.
 // The device work of one TR gradient after the host-side preparation: forward with shell
 // record, adjoint source, interleaved adjoint + replay with the correlation into c.grad.
@@ -1010,10 +1083,20 @@ void gradient_core(Ctx& c, int thickness, bool accumulate) {
     // buffered: adjoint step n writes P[n&1] once replay step n-2 (its last reader) is done.
     // Profiling serialises both on one stream so per-launch event times stay meaningful.
     const bool dual = !c.profiling && c.stream2 != nullptr;
+    const bool green = dual && c.gstream[0] != nullptr;
     cudaStream_t sa = c.stream, sb = dual ? c.stream2 : c.stream;
     float* P[2] = {adj.p, c.adj_p2};
     if (dual) {
         CK(cudaEventRecord(c.ev_fork, sa));
+        if (green) {
+            // the adjoint and the replay each on their own SM partition (persistent pencil
+            // grids sized to the partition); the caller's stream joins both at the end
+            sa = c.gstream[0];
+            sb = c.gstream[1];
+            CK(cudaStreamWaitEvent(sa, c.ev_fork, 0));
+            adj.pgrid = 2 * c.gsm[0];
+            rep.pgrid = 2 * c.gsm[1];
+        }
         CK(cudaStreamWaitEvent(sb, c.ev_fork, 0));
     }
 
@@ -1055,7 +1138,7 @@ void gradient_core(Ctx& c, int thickness, bool accumulate) {
         const char* e = std::getenv("USTFWI_PAIR_LAG");
         return e ? std::atoi(e) : 0;
     }();
-    if (dual && pair_grid > 0) {
+    if (dual && !green && pair_grid > 0) {
         int nsm = 0;
         CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
         adj.pgrid = rep.pgrid = pair_grid * nsm;
@@ -1065,6 +1148,7 @@ void gradient_core(Ctx& c, int thickness, bool accumulate) {
     if (dual && pair_lag) {
         aio.lag_rec = c.ev_lag;
         rio.lag_wait = c.ev_lag;
+        rio.lag_off = pair_lag - 1;  // USTFWI_PAIR_LAG=m: the replay trails by m-1 passes more
     }
     const float inv_dt = static_cast<float>(1.0 / c.grid.dt);
     for (int n = 1; n <= last - 1; ++n) {
@@ -1093,6 +1177,10 @@ void gradient_core(Ctx& c, int thickness, bool accumulate) {
     if (dual) {
         CK(cudaEventRecord(c.ev_join, sb));
         CK(cudaStreamWaitEvent(sa, c.ev_join, 0));
+        if (green) {
+            CK(cudaEventRecord(c.ev_gjoin, sa));
+            CK(cudaStreamWaitEvent(c.stream, c.ev_gjoin, 0));
+        }
     }
     adj.pgrid = rep.pgrid = 0;
 }
@@ -1276,6 +1364,22 @@ int ustfwi_gpu_create(int device, const ustfwi_grid* grid, ustfwi_gpu_ctx** out)
         }
         CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_a));
         CK(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, prio_b));
+        {
+            // SM-partitioned pair loop: the replay (the heavier stream: it also correlates)
+            // on 54 % of the SMs, rounded up to the driver's granularity of 8 (80 of 148),
+            // the adjoint on the rest. USTFWI_GREEN=0 disables it, =k asks for k replay SMs.
+            const char* e = std::getenv("USTFWI_GREEN");
+            const bool forced = e != nullptr;
+            const int want = forced ? std::atoi(e) : (prop.multiProcessorCount * 54 + 99) / 100;
+            if (want > 0 && want < prop.multiProcessorCount) {
+                try {
+                    green_partition(*c, want, prio_a, prio_b);
+                } catch (const std::exception&) {
+                    if (forced) throw;
+                    drop_green(*c);  // e.g. no green-context support: shared-SM streams
+                }
+            }
+        }
         for (int k = 0; k < 2; ++k) {
             CK(cudaEventCreateWithFlags(&c->ev_adj[k], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&c->ev_rep[k], cudaEventDisableTiming));
@@ -1418,6 +1522,7 @@ void ustfwi_gpu_destroy(ustfwi_gpu_ctx* c) {
     for (cudaEvent_t e : c->ev_lag)
         if (e) cudaEventDestroy(e);
     for (void* p : c->allocs) cudaFree(p);
+    drop_green(*c);
     if (c->stream2) {
         cudaStreamSynchronize(c->stream2);
         cudaStreamDestroy(c->stream2);
