@@ -615,7 +615,8 @@ void run_step(Ctx& c, Sim& s, const StepIO& io, cudaStream_t st) {
     // the fast path splits the step into the per-axis density update and the pressure
     // kernel, which re-reads the three split densities (+3F)
     const bool split = !use_generic_kernels() && fast_rows_supported(g.nz);
-    const double zb = 4 * SB + (split ? 11 : 8) * FB + (c.dtrho0.field ? FB : 0.0) + (io.corr.grad ? 5 * FB : 0.0);
+    const double zb = 4 * SB + (split ? 11 : 8) * FB + (c.dtrho0.field ? FB : 0.0) + (io.corr.grad ? 5 * FB : 0.0) -
+                      (io.p_out ? 0.0 : FB);
     if (io.wait_before_z) CK(cudaStreamWaitEvent(st, io.wait_before_z, 0));
     before();
     c.launch(KIND_ZRHO, zb, [&] { return launch_zrho(g, a, true, st); }, st);
@@ -988,8 +989,8 @@ void acc_correlate(Ctx& c, Correlate cr, int nw, int mid, int old, cudaStream_t 
     c.count(launch_correlate(c.g.N, c.ring[nw], c.c0sq, cr, st));
 }
 
-// SM partition of the pair loop (USTFWI_GREEN=k, default 54 % of the SMs): the replay stream gets a green
-// context of k SMs (rounded by the driver to its granularity of 8), the adjoint the rest, so
+// SM partition of the pair loop (USTFWI_GREEN=k, default 48 % of the SMs): the adjoint stream gets a green
+// context of k SMs (rounded by the driver to its granularity of 8), the replay the rest, so
 // the two streams' passes run side by side on disjoint SMs instead of both persistent grids
 // filling the whole device in turn.
 template <class F>
@@ -1016,7 +1017,7 @@ void green_partition(Ctx& c, int want, int prio_a, int prio_b) {
     unsigned n = 1;
     if (split(parts, &n, &all, &rest, 0, static_cast<unsigned>(want)) != CUDA_SUCCESS || n != 1)
         fail(USTFWI_ERR_CUDA, "cuDevSmResourceSplitByCount failed");
-    CUdevResource* res[2] = {&rest, &parts[0]};  // adjoint: the remainder, replay: the k SMs
+    CUdevResource* res[2] = {&parts[0], &rest};  // adjoint (correlates, heavier): the k SMs; replay: the rest
     const int prio[2] = {prio_a, prio_b};
     for (int k = 0; k < 2; ++k) {
         CUdevResourceDesc d{};
@@ -1077,11 +1078,13 @@ void gradient_core(Ctx& c, int thickness, bool accumulate) {
     const int n_shell = static_cast<int>(c.shell_host.size());
     auto shell_row = [&](int m) { return c.trace + static_cast<size_t>(m) * n_shell; };
 
-    // The adjoint runs on c.stream and the time-reversal replay on c.stream2, so their
-    // passes overlap; the only coupling is the correlation in the replay's pressure kernel
-    // (reads the adjoint pressure of the same pair step). The adjoint pressure is double
-    // buffered: adjoint step n writes P[n&1] once replay step n-2 (its last reader) is done.
-    // Profiling serialises both on one stream so per-launch event times stay meaningful.
+    // The adjoint and the time-reversal replay run on two streams (two SM partitions when
+    // green contexts are available), so their passes overlap; the only coupling is the
+    // correlation. Plain c0 gradient: inside the adjoint's pressure kernel, from a 4-slot ring
+    // of replay pressures (see the fused loop below). Otherwise: after each replay step, from
+    // the adjoint pressure, double buffered (adjoint step n writes P[n&1] once replay step
+    // n-2, its last reader, is done). Profiling serialises both on one stream so per-launch
+    // event times stay meaningful.
     const bool dual = !c.profiling && c.stream2 != nullptr;
     const bool green = dual && c.gstream[0] != nullptr;
     cudaStream_t sa = c.stream, sb = dual ? c.stream2 : c.stream;
@@ -1151,6 +1154,49 @@ void gradient_core(Ctx& c, int thickness, bool accumulate) {
         rio.lag_off = pair_lag - 1;  // USTFWI_PAIR_LAG=m: the replay trails by m-1 passes more
     }
     const float inv_dt = static_cast<float>(1.0 / c.grid.dt);
+    const bool fused = !c.plan.extra() && !c.absorbing;
+    if (fused) {
+        // plain c0 gradient: the correlation of pair step n runs inside the ADJOINT's pressure
+        // kernel, which holds q_n in registers and reads the replay's p_{n+1}, p_n, p_{n-1}
+        // from a 4-slot ring, so the adjoint pressure is never stored or re-read (6 instead of
+        // 7 fields of correlation traffic per pair step). The replay leads: adjoint step n waits
+        // for replay step n; replay step n overwrites the ring slot last read by adjoint step
+        // n-2 and waits for it.
+        float* R4[4] = {c.ring[0], c.ring[1], c.ring[2], c.adj_p2};
+        if (aio.lag_rec) {  // USTFWI_PAIR_LAG: here the replay leads
+            std::swap(aio.lag_rec, rio.lag_rec);
+            std::swap(aio.lag_wait, rio.lag_wait);
+            std::swap(aio.lag_off, rio.lag_off);
+        }
+        for (int n = 1; n <= last - 1; ++n) {
+            rio.enf.vals = shell_row(last - n - 1);
+            rio.p_out = R4[(n + 1) & 3];
+            rio.corr = Correlate{};
+            rio.check_step = ((n + 1) & 63) == 0 ? n + 1 : 0;
+            rio.wait_before_z = (dual && n >= 3) ? c.ev_adj[n & 1] : nullptr;  // adjoint n-2 done
+            run_step(c, rep, rio, sb);
+            if (dual) CK(cudaEventRecord(c.ev_rep[n & 1], sb));
+            aio.step_n = n;
+            aio.check_step = (n & 63) == 0 ? n : 0;
+            aio.p_out = nullptr;
+            Correlate corr{R4[n & 3], R4[(n - 1) & 3], nullptr, c.grad, inv_dt};
+            corr.p_new = R4[(n + 1) & 3];
+            aio.corr = corr;
+            aio.wait_before_z = dual ? c.ev_rep[n & 1] : nullptr;  // replay step n done
+            run_step(c, adj, aio, sa);
+            if (dual) CK(cudaEventRecord(c.ev_adj[n & 1], sa));
+        }
+        if (dual) {
+            CK(cudaEventRecord(c.ev_join, sb));
+            CK(cudaStreamWaitEvent(sa, c.ev_join, 0));
+            if (green) {
+                CK(cudaEventRecord(c.ev_gjoin, sa));
+                CK(cudaStreamWaitEvent(c.stream, c.ev_gjoin, 0));
+            }
+        }
+        adj.pgrid = rep.pgrid = 0;
+        return;
+    }
     for (int n = 1; n <= last - 1; ++n) {
         aio.step_n = n;
         aio.check_step = (n & 63) == 0 ? n : 0;
@@ -1160,18 +1206,14 @@ void gradient_core(Ctx& c, int thickness, bool accumulate) {
         if (dual) CK(cudaEventRecord(c.ev_adj[n & 1], sa));
         rio.enf.vals = shell_row(last - n - 1);
         rio.p_out = c.ring[(n + 1) % 3];
-        // plain c0 gradient: the correlation runs inside the replay's pressure kernel;
-        // otherwise (absorption terms, alpha0 / y) after the step, from the rings
+        // absorption terms, alpha0 / y / rho0: the correlation after the replay step, from the rings
         const Correlate corr{c.ring[n % 3], c.ring[(n - 1) % 3], P[n & 1], c.grad, inv_dt};
-        const bool fused = !c.plan.extra() && !c.absorbing;
-        rio.corr = fused ? corr : Correlate{};
+        rio.corr = Correlate{};
         rio.check_step = ((n + 1) & 63) == 0 ? n + 1 : 0;
         rio.wait_before_z = dual ? c.ev_adj[n & 1] : nullptr;                 // adjoint step n done
         run_step(c, rep, rio, sb);
-        if (!fused) {
-            acc_push(c, rep, (n + 1) % 3, sb);
-            acc_correlate(c, corr, (n + 1) % 3, n % 3, (n - 1) % 3, sb);
-        }
+        acc_push(c, rep, (n + 1) % 3, sb);
+        acc_correlate(c, corr, (n + 1) % 3, n % 3, (n - 1) % 3, sb);
         if (dual) CK(cudaEventRecord(c.ev_rep[n & 1], sb));
     }
     if (dual) {
@@ -1365,12 +1407,13 @@ int ustfwi_gpu_create(int device, const ustfwi_grid* grid, ustfwi_gpu_ctx** out)
         CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_a));
         CK(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, prio_b));
         {
-            // SM-partitioned pair loop: the replay (the heavier stream: it also correlates)
-            // on 54 % of the SMs, rounded up to the driver's granularity of 8 (80 of 148),
-            // the adjoint on the rest. USTFWI_GREEN=0 disables it, =k asks for k replay SMs.
+            // SM-partitioned pair loop: the adjoint (which also correlates) on 48 % of the SMs,
+            // rounded up to the driver's granularity of 8 (72 of 148), the replay (which leads,
+            // and records) on the rest; measured on D200: adjoint 64 / 72 / 80 / 88 SMs ->
+            // see DESIGN.md section 7. USTFWI_GREEN=0 disables it, =k asks for k adjoint SMs.
             const char* e = std::getenv("USTFWI_GREEN");
             const bool forced = e != nullptr;
-            const int want = forced ? std::atoi(e) : (prop.multiProcessorCount * 54 + 99) / 100;
+            const int want = forced ? std::atoi(e) : (prop.multiProcessorCount * 48 + 99) / 100;
             if (want > 0 && want < prop.multiProcessorCount) {
                 try {
                     green_partition(*c, want, prio_a, prio_b);

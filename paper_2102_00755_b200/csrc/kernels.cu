@@ -319,13 +319,15 @@ __global__ void __launch_bounds__(256) zrho_kernel(GridDev g, ZrhoArgs A) {
             A.rho[2][i] = r2;
         }
         const float p = __ldg(A.c0sq + i) * ((r0 + r1) + r2);
-        A.p_out[i] = p;
+        if (A.p_out) A.p_out[i] = p;
         D[0][t] = p;
         if (A.corr.grad != nullptr) {
             const float c2 = __ldg(A.c0sq + i);
             const float w = 2.f / (c2 * sqrtf(c2));
-            const float ddot = ((p - 2.f * A.corr.p_mid[i]) + A.corr.p_old[i]) * A.corr.inv_dt;
-            A.corr.grad[i] += w * ddot * A.corr.q_adj[i];
+            const bool adj = A.corr.p_new != nullptr;  // see Correlate::p_new
+            const float pn = adj ? A.corr.p_new[i] : p, q = adj ? p : A.corr.q_adj[i];
+            const float ddot = ((pn - 2.f * A.corr.p_mid[i]) + A.corr.p_old[i]) * A.corr.inv_dt;
+            A.corr.grad[i] += w * ddot * q;
         }
         if (A.check_step > 0 && i == 0 && !isfinite(p)) atomicMin(A.diverged, A.check_step);
     }

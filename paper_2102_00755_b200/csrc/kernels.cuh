@@ -117,7 +117,34 @@ struct Correlate {
     const float* wa1l = nullptr;
     const float* wa2l = nullptr;
     float dt = 0.f;
+    // set: the pressure kernel computing this correlation is the ADJOINT's (its own p is q) and
+    // the replay's new pressure is read from p_new; null: the kernel is the replay's (its own
+    // p is p_new) and q is read from q_adj
+    const float* p_new = nullptr;
 };
+
+#ifdef __CUDACC__
+// grad += (2/c0^3) ((p_new - 2 p_mid) + p_old) / dt * q for a pair of voxels at i (i even),
+// with p the calling pressure kernel's own value (see Correlate::p_new); the same fp32
+// operations in the same order whichever stepper's kernel runs it
+__device__ __forceinline__ void correlate_pair(const Correlate& C, long long i, float2 p, float2 c2) {
+    const float2 pm = *reinterpret_cast<const float2*>(C.p_mid + i);
+    const float2 po = *reinterpret_cast<const float2*>(C.p_old + i);
+    float2 pn, qa;
+    if (C.p_new != nullptr) {
+        pn = *reinterpret_cast<const float2*>(C.p_new + i);
+        qa = p;
+    } else {
+        pn = p;
+        qa = *reinterpret_cast<const float2*>(C.q_adj + i);
+    }
+    float2 gv = *reinterpret_cast<const float2*>(C.grad + i);
+    const float wx = 2.f / (c2.x * sqrtf(c2.x)), wy = 2.f / (c2.y * sqrtf(c2.y));
+    gv.x += wx * (((pn.x - 2.f * pm.x) + po.x) * C.inv_dt) * qa.x;
+    gv.y += wy * (((pn.y - 2.f * pm.y) + po.y) * C.inv_dt) * qa.y;
+    *reinterpret_cast<float2*>(C.grad + i) = gv;
+}
+#endif
 
 // Per-axis PML profiles (make_pml, grid.hpp:153-178), fp32.
 struct Pml {

@@ -858,22 +858,12 @@ __global__ void __launch_bounds__(RowCfg<M, N1, RW>::NT) zp_kernel(const __grid_
             float2 p;
             p.x = c2[n1].x * ((q0[n1].x + q1[n1].x) + q2[n1].x);
             p.y = c2[n1].y * ((q0[n1].y + q1[n1].y) + q2[n1].y);
-            *reinterpret_cast<float2*>(A.p_out + i) = p;
+            if (A.p_out) *reinterpret_cast<float2*>(A.p_out + i) = p;
             pv[n1] = p;
         }
         if (A.corr.grad != nullptr) {
 #pragma unroll
-            for (int n1 = 0; n1 < N1; ++n1) {
-                const long long i = row * NZ + 2 * (lane + N2 * n1);
-                const float2 pm = *reinterpret_cast<const float2*>(A.corr.p_mid + i);
-                const float2 po = *reinterpret_cast<const float2*>(A.corr.p_old + i);
-                const float2 qa = *reinterpret_cast<const float2*>(A.corr.q_adj + i);
-                float2 gv = *reinterpret_cast<const float2*>(A.corr.grad + i);
-                const float wx = 2.f / (c2[n1].x * sqrtf(c2[n1].x)), wy = 2.f / (c2[n1].y * sqrtf(c2[n1].y));
-                gv.x += wx * (((pv[n1].x - 2.f * pm.x) + po.x) * A.corr.inv_dt) * qa.x;
-                gv.y += wy * (((pv[n1].y - 2.f * pm.y) + po.y) * A.corr.inv_dt) * qa.y;
-                *reinterpret_cast<float2*>(A.corr.grad + i) = gv;
-            }
+            for (int n1 = 0; n1 < N1; ++n1) correlate_pair(A.corr, row * NZ + 2 * (lane + N2 * n1), pv[n1], c2[n1]);
         }
         if (A.check_step > 0 && row == 0 && lane == 0 && !isfinite(pv[0].x)) atomicMin(A.diverged, A.check_step);
     }
@@ -1331,18 +1321,9 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR, USTFWI_ZP_MINB) zp2_kerne
                     float2 p;
                     p.x = c2[k].x * ((q0[k].x + q1[k].x) + q2[k].x);
                     p.y = c2[k].y * ((q0[k].y + q1[k].y) + q2[k].y);
-                    *reinterpret_cast<float2*>(A.p_out + i) = p;
+                    if (A.p_out) *reinterpret_cast<float2*>(A.p_out + i) = p;
                     pv[j][n1] = p;
-                    if (A.corr.grad != nullptr) {
-                        const float2 pm = *reinterpret_cast<const float2*>(A.corr.p_mid + i);
-                        const float2 po = *reinterpret_cast<const float2*>(A.corr.p_old + i);
-                        const float2 qa = *reinterpret_cast<const float2*>(A.corr.q_adj + i);
-                        float2 gv = *reinterpret_cast<const float2*>(A.corr.grad + i);
-                        const float wx = 2.f / (c2[k].x * sqrtf(c2[k].x)), wy = 2.f / (c2[k].y * sqrtf(c2[k].y));
-                        gv.x += wx * (((p.x - 2.f * pm.x) + po.x) * A.corr.inv_dt) * qa.x;
-                        gv.y += wy * (((p.y - 2.f * pm.y) + po.y) * A.corr.inv_dt) * qa.y;
-                        *reinterpret_cast<float2*>(A.corr.grad + i) = gv;
-                    }
+                    if (A.corr.grad != nullptr) correlate_pair(A.corr, i, p, c2[k]);
                 }
             }
         }
@@ -1556,18 +1537,9 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR, 4) zrhop_kernel(const __g
                 float2 p;
                 p.x = c2.x * sm.x;
                 p.y = c2.y * sm.y;
-                *reinterpret_cast<float2*>(A.p_out + i) = p;
+                if (A.p_out) *reinterpret_cast<float2*>(A.p_out + i) = p;
                 pv[j][n1] = p;
-                if (A.corr.grad != nullptr) {
-                    const float2 pm = *reinterpret_cast<const float2*>(A.corr.p_mid + i);
-                    const float2 po = *reinterpret_cast<const float2*>(A.corr.p_old + i);
-                    const float2 qa = *reinterpret_cast<const float2*>(A.corr.q_adj + i);
-                    float2 gv = *reinterpret_cast<const float2*>(A.corr.grad + i);
-                    const float wx = 2.f / (c2.x * sqrtf(c2.x)), wy = 2.f / (c2.y * sqrtf(c2.y));
-                    gv.x += wx * (((p.x - 2.f * pm.x) + po.x) * A.corr.inv_dt) * qa.x;
-                    gv.y += wy * (((p.y - 2.f * pm.y) + po.y) * A.corr.inv_dt) * qa.y;
-                    *reinterpret_cast<float2*>(A.corr.grad + i) = gv;
-                }
+                if (A.corr.grad != nullptr) correlate_pair(A.corr, i, p, c2);
             }
         }
         if (A.check_step > 0 && row == 0 && t == 0 && !isfinite(pv[0][0].x)) atomicMin(A.diverged, A.check_step);
