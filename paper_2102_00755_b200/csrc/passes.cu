@@ -1228,8 +1228,12 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const _
 #ifndef USTFWI_ZP_MINB
 #define USTFWI_ZP_MINB 8
 #endif
-template <int M, int N1, int RW>
-__global__ void __launch_bounds__(RW * Z2<M, N1>::TPR, USTFWI_ZP_MINB) zp2_kernel(const __grid_constant__ ZrhoFastArgs P) {
+#ifndef USTFWI_ZPC_MINB
+#define USTFWI_ZPC_MINB 6
+#endif
+template <int M, int N1, int RW, bool CORR>
+__global__ void __launch_bounds__(RW * Z2<M, N1>::TPR, CORR ? USTFWI_ZPC_MINB : USTFWI_ZP_MINB)
+    zp2_kernel(const __grid_constant__ ZrhoFastArgs P) {
     using C = Z2<M, N1>;
     constexpr int N2 = C::N2, TPR = C::TPR, NA = C::NA, NZ = C::NZ, NT = RW * TPR;
     extern __shared__ __align__(128) unsigned char sm_raw[];
@@ -1306,6 +1310,9 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR, USTFWI_ZP_MINB) zp2_kerne
 #pragma unroll
             for (int c0 = 0; c0 < N1; c0 += ZPC) {
                 float2 q0[ZPC], q1[ZPC], q2[ZPC], c2[ZPC];
+                float2 pm[CORR ? ZPC : 1], po[CORR ? ZPC : 1], pq[CORR ? ZPC : 1], gv[CORR ? ZPC : 1];
+                // correlation: the replay's p_new (adjoint kernel) or q (replay kernel)
+                const float* other = CORR ? (A.corr.p_new ? A.corr.p_new : A.corr.q_adj) : nullptr;
 #pragma unroll
                 for (int k = 0; k < ZPC; ++k) {
                     const long long i = row * NZ + 2 * (n2 + N2 * (c0 + k));
@@ -1313,6 +1320,12 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR, USTFWI_ZP_MINB) zp2_kerne
                     q1[k] = *reinterpret_cast<const float2*>(A.rho[1] + i);
                     q2[k] = *reinterpret_cast<const float2*>(A.rho[2] + i);
                     c2[k] = __ldg(reinterpret_cast<const float2*>(A.c0sq + i));
+                    if constexpr (CORR) {  // issued with the stream loads, before any store
+                        pm[k] = *reinterpret_cast<const float2*>(A.corr.p_mid + i);
+                        po[k] = *reinterpret_cast<const float2*>(A.corr.p_old + i);
+                        pq[k] = *reinterpret_cast<const float2*>(other + i);
+                        gv[k] = *reinterpret_cast<const float2*>(A.corr.grad + i);
+                    }
                 }
 #pragma unroll
                 for (int k = 0; k < ZPC; ++k) {
@@ -1323,7 +1336,16 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR, USTFWI_ZP_MINB) zp2_kerne
                     p.y = c2[k].y * ((q0[k].y + q1[k].y) + q2[k].y);
                     if (A.p_out) *reinterpret_cast<float2*>(A.p_out + i) = p;
                     pv[j][n1] = p;
-                    if (A.corr.grad != nullptr) correlate_pair(A.corr, i, p, c2[k]);
+                    if constexpr (CORR) {
+                        // correlate_pair with the loads hoisted: the same fp32 operations
+                        const bool adj = A.corr.p_new != nullptr;
+                        const float2 pn = adj ? pq[k] : p, qa = adj ? p : pq[k];
+                        const float wx = 2.f / (c2[k].x * sqrtf(c2[k].x)), wy = 2.f / (c2[k].y * sqrtf(c2[k].y));
+                        float2 g2 = gv[k];
+                        g2.x += wx * (((pn.x - 2.f * pm[k].x) + po[k].x) * A.corr.inv_dt) * qa.x;
+                        g2.y += wy * (((pn.y - 2.f * pm[k].y) + po[k].y) * A.corr.inv_dt) * qa.y;
+                        *reinterpret_cast<float2*>(A.corr.grad + i) = g2;
+                    }
                 }
             }
         }
@@ -2284,7 +2306,7 @@ cudaError_t zrho2_run(const GridDev& g, const ZrhoFastArgs& a, cudaStream_t st) 
     kern<<<blocks, RW * Z2<M, N1>::TPR, smem, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    auto kp = zp2_kernel<M, N1, RW>;
+    auto kp = a.a.corr.grad ? zp2_kernel<M, N1, RW, true> : zp2_kernel<M, N1, RW, false>;
     const size_t smem_p = (size_t(M) + size_t(RW) * Z2<M, N1>::ZT) * sizeof(float2);
     cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
     kp<<<blocks.x, RW * Z2<M, N1>::TPR, smem_p, st>>>(a);
