@@ -1577,7 +1577,21 @@ void ustfwi_gpu_destroy(ustfwi_gpu_ctx* c) {
 int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho0, const double* alpha0, double y,
                           const uint8_t* gamma, double c0_min, double c0_max) {
     return guarded(c, [&] {
-        c->touch();
+        // what a captured gradient graph bakes in from the medium: the density coefficients
+        // (scalars when rho0 is uniform), the absorption plan, the exponent, the shell. A new
+        // medium that leaves all of them unchanged (an optimizer iterate: new c0 values in
+        // place) keeps the graph; anything else invalidates it
+        const bool prev_plain = c->has_medium && !c->absorbing && c->dtr_fields == nullptr;
+        const Coef prev_dtrho0 = c->dtrho0;
+        const Coef prev_stag[3] = {c->dtr_stag[0], c->dtr_stag[1], c->dtr_stag[2]};
+        const double prev_y = c->y_pow;
+        struct Invalidate {  // on every exit (errors included) unless the graph is known valid
+            Ctx* c;
+            bool keep = false;
+            ~Invalidate() {
+                if (!keep) c->touch();
+            }
+        } inval{c};
         const size_t N = static_cast<size_t>(c->g.N);
         if (!c0 || !rho0) fail(USTFWI_ERR_INVALID, "medium fields must match the grid");
         // Medium::validate (medium.hpp:41-57); chunked over host threads, the first failing
@@ -1700,6 +1714,11 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
         }
         c->has_medium = true;
         CK(cudaStreamSynchronize(c->stream));
+        const bool same_coef = uniform_rho && prev_dtrho0.scalar == c->dtrho0.scalar &&
+                               prev_stag[0].scalar == c->dtr_stag[0].scalar &&
+                               prev_stag[1].scalar == c->dtr_stag[1].scalar && prev_stag[2].scalar == c->dtr_stag[2].scalar;
+        inval.keep = prev_plain && !absorbing && same_coef && prev_y == y && same_gamma &&
+                     c->grad_param == USTFWI_PARAM_C0;
     });
 }
 
@@ -1771,6 +1790,8 @@ int ustfwi_gpu_set_sensors(ustfwi_gpu_ctx* c, size_t n_sensors, const size_t* po
         std::vector<size_t> p(pos, pos + n_sensors);
         for (size_t v : p)
             if (v >= N) fail(USTFWI_ERR_INVALID, "sensor position outside grid");
+        if (c->sens_pos && c->data && c->n_sens == static_cast<int>(n_sensors) && c->sens_pos_host == p)
+            return;  // the bound sensor array: nothing to rebind (a captured graph stays valid)
         c->n_sens = static_cast<int>(n_sensors);
         c->sens_pos_host = p;
         std::vector<int> order(n_sensors);

@@ -204,7 +204,7 @@ class GpuEngine:
                     param: str = "c0"):
         """-> (loss, grad) ; grad zero outside gamma. dispersion_enabled: GradientOptions
         (gradient.hpp:31), the adjoint / replay dispersion term of absorbing media; param:
-        GradientParam c0 | alpha0 | y (gradient.hpp:9; rho0 is rejected)."""
+        GradientParam c0 | rho0 | alpha0 | y (gradient.hpp:9)."""
         obs = np.ascontiguousarray(observed, dtype=np.float64)
         if obs.shape != (self.n_sensors, self.grid.nt):
             raise ValueError("observed data dimensions do not match the simulation")

@@ -38,3 +38,43 @@ def test_graph_replay_is_bit_identical_to_eager():
         l2, g2 = eng.download_gradient()
     assert g1.tobytes() == g2.tobytes() and l1 == l2
     assert np.linalg.norm(g1 - 0.25 * res[0][1]) <= 1e-5 * np.linalg.norm(g1)
+
+
+def test_new_c0_values_reuse_the_graph_correctly():
+    """An optimizer iterate: set_medium with new c0 values but the same structure (uniform
+    rho0, no absorption, same gamma) keeps the captured graph (the c0^2 field is updated in
+    place); the result must equal a fresh engine's for the new medium, bit for bit. A new
+    uniform rho0 value (baked into the launches as a scalar) must invalidate it."""
+    from paper_2102_00755_b200.engine import Medium
+    sc = scenario.config_a(nt=96)
+    obs = np.zeros((len(sc.sensors.positions), sc.grid.nt))
+    m = sc.model
+    c0b = np.asarray(m.c0) * (1.0 + 0.01 * np.sin(np.arange(np.asarray(m.c0).size)).reshape(np.shape(m.c0)))
+    c0b = np.clip(c0b, m.c0_min, m.c0_max)
+    mb = Medium(c0=c0b, rho0=m.rho0, gamma=m.gamma, c0_min=m.c0_min, c0_max=m.c0_max)
+    mr = Medium(c0=c0b, rho0=np.asarray(m.rho0) * 1.05, gamma=m.gamma, c0_min=m.c0_min, c0_max=m.c0_max)
+
+    def fresh(medium):
+        with GpuEngine(sc.grid) as e:
+            e.set_medium(medium)
+            e.set_sources(sc.encoded(0))
+            e.set_sensors(sc.sensors)
+            return e.gradient_tr(obs, 8)
+
+    want_b, want_r = fresh(mb), fresh(mr)
+    with GpuEngine(sc.grid) as eng:
+        eng.set_medium(m)
+        eng.set_sources(sc.encoded(0))
+        eng.set_sensors(sc.sensors)
+        for _ in range(3):          # eager, capture, replay
+            eng.gradient_tr(obs, 8)
+        eng.set_medium(mb)
+        eng.set_sensors(sc.sensors)  # the same array: no rebinding
+        got_b = [eng.gradient_tr(obs, 8) for _ in range(2)]
+        eng.set_medium(mr)
+        got_r = [eng.gradient_tr(obs, 8) for _ in range(3)]
+    for loss, grad in got_b:
+        assert loss == want_b[0] and grad.tobytes() == want_b[1].tobytes()
+    for loss, grad in got_r:
+        assert loss == want_r[0] and grad.tobytes() == want_r[1].tobytes()
+    assert want_b[1].tobytes() != want_r[1].tobytes()
