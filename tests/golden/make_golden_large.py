@@ -8,6 +8,7 @@ Run here (where /root/reference exists), one fixture per process (hours of fp64 
     python tests/golden/make_golden_large.py drift   # config A geometry at nt = 3912 (fp32 drift over 3*3912 steps)
     python tests/golden/make_golden_large.py rho0    # config A (nt = 393), heterogeneous rho0: rho0 and c0 gradients
     python tests/golden/make_golden_large.py Dgrad   # config-D grid, 16 + 16 transducers next to Gamma, nt = 100 TR gradient
+    python tests/golden/make_golden_large.py E0      # config E level 0 (2 mm, 144x144x96), full nt = 978, observed = 0
 
 Every input is built exactly as bench.py / scenario.py build it (same seeds, same encoding
 realization r = 0 of master seed 20210201, tau = 0), so the device run in
@@ -74,6 +75,12 @@ def gradient_fixture(sc, name, r=0, observed_zero=False):
 
 def config_b_fixture():
     gradient_fixture(scenario.config_b(), "config_b")
+
+
+def config_e0_fixture():
+    # the 2 mm multigrid level at its full nt = 978: 144 x 144 x 96 (the 144-point pencils and
+    # the nz = 96 z kernels), 64 encoded emitters; observed = 0 (the residual is the model data)
+    gradient_fixture(scenario.config_e(0), "config_e0", observed_zero=True)
 
 
 def drift_fixture():
@@ -152,4 +159,4 @@ if __name__ == "__main__":
         sys.exit("oracle/_ref missing: make -C oracle")
     which = sys.argv[1] if len(sys.argv) > 1 else ""
     {"B": config_b_fixture, "D": config_d_fixture, "drift": drift_fixture, "rho0": rho0_fixture,
-     "Dgrad": config_d_gradient_fixture}[which]()
+     "Dgrad": config_d_gradient_fixture, "E0": config_e0_fixture}[which]()

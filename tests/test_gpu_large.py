@@ -9,6 +9,7 @@ produced (oracle/_ref, tests/golden/make_golden_large.py; hours of fp64 CPU work
       per-step shell-trace |sums|, the shell-trace subsample on the field's scale;
   fp32 drift, config A geometry at nt = 3912 (the config-D step count): traces and TR gradient
       after 3 * 3912 - 3 steps;
+  config E level 0 (2 mm, 144 x 144 x 96) at its full nt = 978: traces and TR gradient;
   the TR gradient on the config-D grid (scenario.config_d_gradient_problem: the bench phantom,
       16 + 16 transducers next to Gamma so that 100 steps already cross the 1.16 M-voxel shell).
 
@@ -66,6 +67,19 @@ def test_config_b_full_nt_matches_reference(golden):
     assert r["traces"] < TRACE_TOL
     assert r["trace_abs"] < TRACE_TOL and r["trace_sq"] < 2 * TRACE_TOL and r["trace_sum"] < TRACE_TOL
     assert r["loss"] < TRACE_TOL
+    assert r["grad"] < GRAD_TOL and r["grad_outside"] == 0.0
+
+
+def test_config_e0_full_nt_matches_reference(golden):
+    """The 2 mm multigrid level (144 x 144 x 96: 144-point pencils, the nz = 96 z kernels) at
+    its full nt = 978, 64 encoded emitters, observed = 0."""
+    z = load(golden, "config_e0")
+    sc = scenario.config_e(0)
+    assert sc.grid.nt == int(z["nt"]) == 978
+    r = gradient_parity(sc, z)
+    print("config E0:", r)
+    assert r["traces"] < TRACE_TOL and r["loss"] < TRACE_TOL
+    assert r["trace_abs"] < TRACE_TOL and r["trace_sq"] < 2 * TRACE_TOL
     assert r["grad"] < GRAD_TOL and r["grad_outside"] == 0.0
 
 
