@@ -448,11 +448,11 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
                 // forward x FFT then kappa (all jobs of a source share its kappa flag); kappa of
                 // the tile is evaluated once (first source group) into thread-private slots
                 forward(X);
-                if (inB && jobs.job[gb].kappa) {
-                    if (grp == 0) {
+                const int kind = jobs.job[gb].kappa;  // one multiplier kind per launch (CTA-uniform)
+                if (kind && grp == 0) {
+                    if (inB) {
                         const float ky = g.ky[line];
                         const float kz = col0 + c < g.nzh ? g.kz[col0 + c] : 0.f;
-                        const int kind = jobs.job[gb].kappa;  // one multiplier kind per launch
                         const bool power = kind >= 2;
                         const float e = jobs.job[gb].kexp;
                         if (power) {
@@ -462,18 +462,27 @@ __global__ void __launch_bounds__(PencilCfg<L, N1, TB, DB>::NT, MINB)
                                 kap_s[k * TB + c] = kpow_mult_call(kx * kx + ky * ky + kz * kz, e, kind);
                             }
                         } else {
-                            // u = (h kx)^2 + (h ky)^2 + (h kz)^2, the x term from the shared table
+                            // u = (h kx)^2 + (h ky)^2 + (h kz)^2, the x term from the shared table;
+                            // kx^2 is even in k (kx[L-k] = -kx[k]), so kappa is evaluated for
+                            // rows k <= L/2 only and mirrored through shared memory
                             const float hy = g.half_cdt * ky, hz = g.half_cdt * kz;
                             const float uyz = hy * hy + hz * hz;
 #pragma unroll
                             for (int k2 = 0; k2 < N2; ++k2) {
                                 const int k = C::out_row(kb, k2);
-                                kap_s[k * TB + c] = kappa_of_u(hkx2_s[k] + uyz);
+                                if (k <= L / 2) kap_s[k * TB + c] = kappa_of_u(hkx2_s[k] + uyz);
                             }
                         }
                     }
+                    if (kind < 2) __syncthreads();  // mirrored entries written by other threads
+                }
+                if (inB && kind) {
 #pragma unroll
-                    for (int k2 = 0; k2 < N2; ++k2) X[k2] = cscale(X[k2], kap_s[C::out_row(kb, k2) * TB + c]);
+                    for (int k2 = 0; k2 < N2; ++k2) {
+                        const int k = C::out_row(kb, k2);
+                        const int km = (kind < 2 && k > L / 2) ? L - k : k;
+                        X[k2] = cscale(X[k2], kap_s[km * TB + c]);
+                    }
                 }
             } else if (inB) {
 #pragma unroll
