@@ -1015,9 +1015,12 @@ void green_partition(Ctx& c, int want, int prio_a, int prio_b) {
     if (get_res(static_cast<CUdevice>(c.device), &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
         fail(USTFWI_ERR_CUDA, "cuDeviceGetDevResource failed");
     unsigned n = 1;
-    if (split(parts, &n, &all, &rest, 0, static_cast<unsigned>(want)) != CUDA_SUCCESS || n != 1)
+    if (split(parts, &n, &all, &rest, 0, static_cast<unsigned>(std::abs(want))) != CUDA_SUCCESS || n != 1)
         fail(USTFWI_ERR_CUDA, "cuDevSmResourceSplitByCount failed");
-    CUdevResource* res[2] = {&parts[0], &rest};  // adjoint (correlates, heavier): the k SMs; replay: the rest
+    // want > 0: the adjoint (which correlates) gets the k SMs, the replay the rest;
+    // want < 0: the replay gets |k|, the adjoint the rest
+    CUdevResource* res[2] = {&parts[0], &rest};
+    if (want < 0) std::swap(res[0], res[1]);
     const int prio[2] = {prio_a, prio_b};
     for (int k = 0; k < 2; ++k) {
         CUdevResourceDesc d{};
@@ -1414,7 +1417,7 @@ int ustfwi_gpu_create(int device, const ustfwi_grid* grid, ustfwi_gpu_ctx** out)
             const char* e = std::getenv("USTFWI_GREEN");
             const bool forced = e != nullptr;
             const int want = forced ? std::atoi(e) : (prop.multiProcessorCount * 48 + 99) / 100;
-            if (want > 0 && want < prop.multiProcessorCount) {
+            if (want != 0 && std::abs(want) < prop.multiProcessorCount) {
                 try {
                     green_partition(*c, want, prio_a, prio_b);
                 } catch (const std::exception&) {
