@@ -781,7 +781,9 @@ void forward_steps(Ctx& c, int thickness) {
     io.inj = c.src.view();
     io.sens = SparseGather{c.n_sens, c.sens_pos, c.sens_idx, nullptr, c.sens_blk8};
     io.shell = SparseGather{n_shell, c.shell_pos, nullptr, nullptr, c.shell_blk8};
-    io.p_out = s.p;
+    // the forward pressure is only gathered (in-kernel, from registers) and transformed into
+    // the next step's S0: not stored, except on the absorbing path, whose tail re-reads it
+    io.p_out = c.absorbing ? s.p : nullptr;
     for (int n = 0; n < nt; ++n) {
         io.step_n = n;
         io.sens.out = c.data + static_cast<size_t>(n) * c.n_sens;
