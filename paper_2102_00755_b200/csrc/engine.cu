@@ -156,6 +156,16 @@ struct ustfwi_gpu_ctx {
     int off_axis = 0;   // 3 - ndim: padded axis of reference axis 0
     GridDev g{};
     std::vector<void*> allocs;
+    float* pinned = nullptr;          // N-float pinned host staging (medium upload, gradient download)
+    float* pinned_stage() {
+        if (!pinned) {
+            void* p = nullptr;
+            if (cudaMallocHost(&p, static_cast<size_t>(g.N) * sizeof(float)) != cudaSuccess)
+                fail(USTFWI_ERR_CUDA, "pinned host staging allocation failed");
+            pinned = static_cast<float*>(p);
+        }
+        return pinned;
+    }
 
     float2* dmul[3][ST_COUNT] = {};  // per padded axis: none / plus / minus / shift +1/2 / shift -1/2 tables
     float* pml_reg[3] = {};
@@ -1570,6 +1580,7 @@ void ustfwi_gpu_destroy(ustfwi_gpu_ctx* c) {
     for (cudaEvent_t e : c->ev_lag)
         if (e) cudaEventDestroy(e);
     for (void* p : c->allocs) cudaFree(p);
+    if (c->pinned) cudaFreeHost(c->pinned);
     drop_green(*c);
     if (c->stream2) {
         cudaStreamSynchronize(c->stream2);
@@ -1649,10 +1660,13 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
             fail(USTFWI_ERR_NUMERICAL, "CFL violation: dt exceeds 2/pi * dx / c_max");
         const double dt = c->grid.dt;
         c->c0_host.resize(N);
-        std::vector<float> c2(N);
+        c->rho0_host.resize(N);
+        CK(cudaStreamSynchronize(c->stream));  // the pinned staging buffer may be in flight
+        float* c2 = c->pinned_stage();
         std::atomic<bool> uniform_ok{true};
         ustfwi_host::parallel_chunks(N, [&](size_t b, size_t e) {
             std::memcpy(c->c0_host.data() + b, c0 + b, (e - b) * sizeof(double));
+            std::memcpy(c->rho0_host.data() + b, rho0 + b, (e - b) * sizeof(double));
             bool u = true;
             for (size_t i = b; i < e; ++i) {
                 c2[i] = static_cast<float>(c0[i] * c0[i]);
@@ -1660,7 +1674,7 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
             }
             if (!u) uniform_ok = false;
         });
-        CK(cudaMemcpyAsync(c->c0sq, c2.data(), N * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->c0sq, c2, N * sizeof(float), cudaMemcpyHostToDevice, c->stream));
         const bool uniform_rho = uniform_ok;
         c->release(c->dtr_fields);
         c->dtr_fields = nullptr;
@@ -1701,7 +1715,6 @@ int ustfwi_gpu_set_medium(ustfwi_gpu_ctx* c, const double* c0, const double* rho
             }
         }
         set_absorption(*c, absorbing ? alpha0 : nullptr, y, c0);
-        c->rho0_host.assign(rho0, rho0 + N);
         if (alpha0) c->alpha0_host.assign(alpha0, alpha0 + N);
         else c->alpha0_host.clear();
         // the boundary shell (shell_indices, medium.hpp:168-178) depends on gamma only: keep
@@ -1877,8 +1890,8 @@ int ustfwi_gpu_download_gradient(ustfwi_gpu_ctx* c, double scale_div, double* gr
         const size_t N = static_cast<size_t>(c->g.N);
         if (!(scale_div >= 1.0)) fail(USTFWI_ERR_INVALID, "scale_div must be >= 1");
         if (grad_out) {
-            std::vector<float> h(N);
-            CK(cudaMemcpyAsync(h.data(), c->acc, N * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+            const float* h = c->pinned_stage();
+            CK(cudaMemcpyAsync(c->pinned, c->acc, N * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
             ustfwi_host::parallel_chunks(N, [&](size_t b, size_t e) {
                 for (size_t i = b; i < e; ++i) grad_out[i] = static_cast<double>(h[i]) / scale_div;

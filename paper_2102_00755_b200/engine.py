@@ -192,7 +192,7 @@ class GpuEngine:
         check(lib().ustfwi_gpu_run_gradient(self._h, int(thickness), int(bool(accumulate))))
 
     def download_gradient(self, scale_div: float = 1.0):
-        grad = np.zeros(self.grid.shape)
+        grad = np.empty(self.grid.shape)  # every element is written by the library
         loss = C.c_double(0.0)
         check(lib().ustfwi_gpu_download_gradient(self._h, C.c_double(scale_div), ptr(grad, C.c_double),
                                                  C.byref(loss)))
@@ -212,7 +212,7 @@ class GpuEngine:
             raise ValueError("unknown gradient parameter")
         check(lib().ustfwi_gpu_set_gradient_options(self._h, int(bool(dispersion_enabled))))
         check(lib().ustfwi_gpu_set_gradient_param(self._h, self.PARAMS[param]))
-        grad = np.zeros(self.grid.shape)
+        grad = np.empty(self.grid.shape)  # every element is written by the library
         loss = C.c_double(0.0)
         check(lib().ustfwi_gpu_gradient_tr(self._h, ptr(obs, C.c_double), int(thickness), ptr(grad, C.c_double),
                                            C.byref(loss)))
