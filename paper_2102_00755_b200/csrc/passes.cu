@@ -1240,7 +1240,7 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const _
 #ifndef USTFWI_ZPC_MINB
 #define USTFWI_ZPC_MINB 6
 #endif
-template <int M, int N1, int RW, bool CORR>
+template <int M, int N1, int RW, bool CORR, bool STORE_P>
 __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR, CORR ? USTFWI_ZPC_MINB : USTFWI_ZP_MINB)
     zp2_kernel(const __grid_constant__ ZrhoFastArgs P) {
     using C = Z2<M, N1>;
@@ -1343,7 +1343,7 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR, CORR ? USTFWI_ZPC_MINB : 
                     float2 p;
                     p.x = c2[k].x * ((q0[k].x + q1[k].x) + q2[k].x);
                     p.y = c2[k].y * ((q0[k].y + q1[k].y) + q2[k].y);
-                    if (A.p_out) *reinterpret_cast<float2*>(A.p_out + i) = p;
+                    if constexpr (STORE_P) *reinterpret_cast<float2*>(A.p_out + i) = p;
                     pv[j][n1] = p;
                     if constexpr (CORR) {
                         // correlate_pair with the loads hoisted: the same fp32 operations
@@ -2315,7 +2315,10 @@ cudaError_t zrho2_run(const GridDev& g, const ZrhoFastArgs& a, cudaStream_t st) 
     kern<<<blocks, RW * Z2<M, N1>::TPR, smem, st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    auto kp = a.a.corr.grad ? zp2_kernel<M, N1, RW, true> : zp2_kernel<M, N1, RW, false>;
+    // no pressure store (forward, adjoint): no store in the element loop, so the compiler may
+    // issue later elements' loads early
+    auto kp = a.a.corr.grad ? (a.a.p_out ? zp2_kernel<M, N1, RW, true, true> : zp2_kernel<M, N1, RW, true, false>)
+                            : (a.a.p_out ? zp2_kernel<M, N1, RW, false, true> : zp2_kernel<M, N1, RW, false, false>);
     const size_t smem_p = (size_t(M) + size_t(RW) * Z2<M, N1>::ZT) * sizeof(float2);
     cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
     kp<<<blocks.x, RW * Z2<M, N1>::TPR, smem_p, st>>>(a);
