@@ -231,6 +231,10 @@ USTFWI_API size_t ustfwi_gpu_shell_size(const ustfwi_gpu_ctx* ctx);
  * out[0] CTAs, out[1] units, out[2] deferred tile loads, out[3] dependency-wait cycles,
  * out[4] tile-wait cycles, summed over CTAs since the previous call. */
 USTFWI_API int ustfwi_gpu_chain_stats(uint64_t* out5);
+/* SM partition of the TR gradient's adjoint / replay pair loop (green contexts; no reference
+ * counterpart, the reference runs both steppers on the host thread in turn, gradient.hpp:443-461):
+ * SMs of the adjoint and of the replay stream, 0 / 0 when both share the device. */
+USTFWI_API int ustfwi_gpu_partition(ustfwi_gpu_ctx* ctx, int* adjoint_sms, int* replay_sms);
 /* Enable/disable event timing of every launch and reset the counters. */
 USTFWI_API int ustfwi_gpu_set_profiling(ustfwi_gpu_ctx* ctx, int enable);
 /* Accumulated device time, launch count and algorithmic bytes (minimum HBM traffic of the

@@ -34,7 +34,7 @@ EXPORTS = [
     "ustfwi_gpu_stepper_init", "ustfwi_gpu_stepper_reset", "ustfwi_gpu_stepper_update_velocity_density",
     "ustfwi_gpu_stepper_inject", "ustfwi_gpu_stepper_enforce", "ustfwi_gpu_stepper_refresh_pressure",
     "ustfwi_gpu_stepper_update_pressure", "ustfwi_gpu_stepper_read", "ustfwi_gpu_stepper_gather",
-    "ustfwi_gpu_stepper_step_index", "ustfwi_gpu_chain_stats",
+    "ustfwi_gpu_stepper_step_index", "ustfwi_gpu_chain_stats", "ustfwi_gpu_partition",
     "ustfwi_lbfgs_create", "ustfwi_lbfgs_destroy", "ustfwi_lbfgs_reset", "ustfwi_lbfgs_push", "ustfwi_lbfgs_apply",
     "ustfwi_lbfgs_pairs", "ustfwi_fourier_interpolate", "ustfwi_lowpass_timeseries", "ustfwi_restrict_traces",
 ]

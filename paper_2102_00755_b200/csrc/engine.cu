@@ -2205,6 +2205,13 @@ int ustfwi_gpu_chain_stats(uint64_t* out5) {
     });
 }
 
+int ustfwi_gpu_partition(ustfwi_gpu_ctx* c, int* adjoint_sms, int* replay_sms) {
+    return guarded(c, [&] {
+        if (adjoint_sms) *adjoint_sms = c->gstream[0] ? c->gsm[0] : 0;
+        if (replay_sms) *replay_sms = c->gstream[1] ? c->gsm[1] : 0;
+    });
+}
+
 int ustfwi_nccl_unique_id(char id_out[128]) {
     return guarded(nullptr, [&] {
         NcclUniqueId id;

@@ -238,6 +238,12 @@ class GpuEngine:
     def stream_ptr(self) -> int:
         return int(lib().ustfwi_gpu_stream(self._h) or 0)
 
+    def partition(self):
+        """(adjoint SMs, replay SMs) of the TR pair loop's green contexts; (0, 0) = shared SMs."""
+        a, r = C.c_int(0), C.c_int(0)
+        check(lib().ustfwi_gpu_partition(self._h, C.byref(a), C.byref(r)))
+        return a.value, r.value
+
     def launch_count(self) -> int:
         return int(lib().ustfwi_gpu_launch_count(self._h))
 

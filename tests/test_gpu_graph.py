@@ -78,3 +78,19 @@ def test_new_c0_values_reuse_the_graph_correctly():
     for loss, grad in got_r:
         assert loss == want_r[0] and grad.tobytes() == want_r[1].tobytes()
     assert want_b[1].tobytes() != want_r[1].tobytes()
+
+
+def test_pair_loop_runs_on_two_sm_partitions():
+    """The adjoint / replay streams of the TR pair loop live in two green contexts with
+    disjoint SM sets (engine.cu green_partition): 48 % of the SMs (a multiple of 8) for the
+    adjoint, the rest for the replay."""
+    import os
+    import torch
+    if "USTFWI_GREEN" in os.environ:
+        pytest.skip("partition overridden by USTFWI_GREEN")
+    n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+    sc = scenario.config_a(nt=24)
+    with GpuEngine(sc.grid) as eng:
+        a, r = eng.partition()
+    assert a > 0 and r > 0 and a + r == n_sm and a % 8 == 0
+    assert a == -(-(n_sm * 48 + 99) // 100 // 8) * 8 or a == (n_sm * 48 + 99) // 100

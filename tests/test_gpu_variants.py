@@ -5,7 +5,8 @@ the nz = 256 z kernels agree across variants (each variant in its own process, t
 are read once). On a 480 x 480 x 32 grid the three separate pencil launches (default) and the
 experimental fused y-x-y chain kernel (USTFWI_CHAIN=1) give the same traces and TR gradient,
 and the eager launches (USTFWI_GRAPH=0) the same as the CUDA-graph replay; the SM-partitioned
-pair loop (USTFWI_GREEN=k, green contexts) the same as the shared-SM one."""
+pair loop (default: green contexts) the same as the shared-SM one (USTFWI_GREEN=0) and as the
+other split (USTFWI_GREEN=-72)."""
 import json
 import os
 import subprocess
@@ -63,7 +64,8 @@ def run(env_extra, layout):
     ("x", {"USTFWI_X480": "1"}), ("x", {"USTFWI_PENCIL_TMA": "0"}),
     ("xy", {"USTFWI_CHAIN": "1"}), ("xy", {"USTFWI_GRAPH": "0"}),
     ("y", {"USTFWI_ZFUSE": "1"}), ("x", {"USTFWI_ZFUSE": "1"}),
-    ("xy", {"USTFWI_GREEN": "72"}), ("xy", {"USTFWI_GREEN": "72", "USTFWI_GRAPH": "0"}),
+    ("xy", {"USTFWI_GREEN": "0"}), ("xy", {"USTFWI_GREEN": "0", "USTFWI_GRAPH": "0"}),
+    ("xy", {"USTFWI_GREEN": "-72"}),
 ])
 def test_kernel_variants_agree(layout, variant):
     base = run({}, layout)
