@@ -18,3 +18,7 @@ python scripts/prof_step.py --config D --nt 4 --grad > gpurun_out/prof_plain_$ta
 ncu --set full --clock-control none --import-source on -k regex:"pencil_|zvel|zrho|zp2_kernel" -s 0 -c 9 \
     -o gpurun_out/prof_full_$tag python scripts/prof_step.py --config D --nt 4 --grad > gpurun_out/ncu_full_$tag.log 2>&1
 echo "ncu full rc=$?"
+# the adjoint's correlating pressure kernel (pair loop only)
+ncu --set full --clock-control none --import-source on -k "regex:zp2_kernel<128, 16, 16, 1" -s 0 -c 1 \
+    -o gpurun_out/prof_corr_$tag python scripts/prof_step.py --config D --nt 4 --grad > gpurun_out/ncu_corr_$tag.log 2>&1
+echo "ncu corr rc=$?"
