@@ -64,9 +64,18 @@ def estimator(eng, sc, base_c0, gam_idx, cache, log):
     return est
 
 
+def arg(name, default):
+    for k, a in enumerate(sys.argv):
+        if a == name and k + 1 < len(sys.argv):
+            return type(default)(sys.argv[k + 1])
+    return default
+
+
 def main():
     out = {"levels": {}}
     quick = "--quick" in sys.argv
+    e1_evals = arg("--e1-evals", 8)       # SLBFGS evaluations on the 1 mm level
+    e1_step = arg("--e1-step", 1.0)       # first step on the 1 mm level, m/s
     levels = () if quick else (0, 1, 2)
     for lv in levels:
         sc = scenario.config_e(lv)
@@ -122,12 +131,12 @@ def main():
         eng.set_sensors(sc1.sensors)
         est = estimator(eng, sc1, c1, gam1, {}, log1)
         F1, G1 = est(c1.ravel()[gam1], 0.0, 1)
-        res1 = slbfgs_run(est, c1.ravel()[gam1], 8, nu=1.0, h0=1.0 / np.abs(G1).max(), bounds=(1350.0, 1800.0),
-                          theta=delay_schedule(b1))
+        res1 = slbfgs_run(est, c1.ravel()[gam1], e1_evals, nu=1.0, h0=e1_step / np.abs(G1).max(),
+                          bounds=(1350.0, 1800.0), theta=delay_schedule(b1))
     c_fine = c1.copy()
     c_fine.ravel()[gam1] = res1.u
     water = np.asarray(sc1.model.c0, dtype=np.float64)
-    hist.append({"level": sc1.name, "evals": res1.n_evl, "energy": res1.energy, "b_s": b1,
+    hist.append({"level": sc1.name, "evals": res1.n_evl, "first_step_m_s": e1_step, "energy": res1.energy, "b_s": b1,
                  "schedule": [(h["iteration"], h["nt_ext"]) for h in log1],
                  "rel_l2_water_init": rel_err(water, np.asarray(sc1.truth.c0), sc1.model.gamma),
                  "rel_l2_prolonged_init": rel_err(c1, np.asarray(sc1.truth.c0), sc1.model.gamma),
