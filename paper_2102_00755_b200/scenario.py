@@ -249,31 +249,38 @@ def encoding_problem(n_src: int, nt: Optional[int] = None):
 
 
 def config_d_gradient_problem():
-    """The config-D grid and phantom with 16 emitters and 16 receivers on rings 6 voxels outside
-    Gamma (z = 40 and 60) and the config-D pulse advanced by 150 samples (peak near sample 52),
-    so that a 100-step gradient already sees the wavefield cross the shell: the full-size parity
-    case of the TR gradient (tests/golden/make_golden_large.py Dgrad, tests/test_gpu_large.py).
-    Returns (scenario with nt = 100, emitters, receivers, pulse)."""
-    sc = config_d(nt=100)
+    """The config-D grid and phantom with 16 emitters on a ring 1 voxel outside Gamma (z = 40)
+    and 16 receivers 2 voxels beside them, nt = 28, the config-D pulse advanced to peak near
+    sample 12, observed data zero: the forward and adjoint fields overlap inside Gamma from
+    about step 8 to 19, so a 28-step TR gradient at the full 480 x 480 x 256 size (the
+    480-point pencils, the nz = 256 rows, the 1.16 M-voxel shell record / replay, the
+    correlation) is non-trivial while the fp64 reference finishes in about 1.5 h
+    (tests/golden/make_golden_large.py Dgrad, tests/test_gpu_large.py).
+    Returns (scenario with nt = 28, emitters, receivers, pulse)."""
+    nt = 28
+    sc = config_d(nt=nt)
     sh = sc.grid.shape
     gam = np.asarray(sc.model.gamma, bool)
     cx = cy = sh[0] // 2
     full = config_d().pulse          # the untruncated pulse of the config-D grid
-    pulse = np.asarray(full[150:250], np.float64)
+    k0 = int(np.argmax(np.abs(full))) - 12
+    pulse = np.asarray(full[k0:k0 + nt], np.float64)
+    z = 40
+    r_g = 0
+    while gam[cx + r_g + 1, cy, z]:
+        r_g += 1
 
-    def ring(z, off):
-        r_g = 0
-        while gam[cx + r_g + 1, cy, z]:
-            r_g += 1
-        rr = r_g + 6
+    def ring(gap, dtheta):
+        rr = r_g + gap
         pts = []
         for k in range(16):
-            th = 2 * np.pi * (k + off) / 16
+            th = 2 * np.pi * k / 16 + dtheta
             x, y = int(round(cx + rr * np.cos(th))), int(round(cy + rr * np.sin(th)))
-            assert not gam[x, y, z]
+            while gam[x, y, z]:  # rounding landed on Gamma: step outwards
+                x, y = int(round(x + np.cos(th))), int(round(y + np.sin(th)))
             pts.append(flat(sh, x, y, z))
         return pts
-    return sc, ring(40, 0.0), ring(60, 0.5), pulse
+    return sc, ring(1, 0.0), ring(1, 2.0 / (r_g + 1)), pulse
 
 
 CONFIGS = {"A": config_a, "B": config_b, "C": config_c, "D": config_d,

@@ -7,7 +7,7 @@ Run here (where /root/reference exists), one fixture per process (hours of fp64 
     python tests/golden/make_golden_large.py D       # config D grid + bench phantom + 1024 encoded emitters, nt = 160
     python tests/golden/make_golden_large.py drift   # config A geometry at nt = 3912 (fp32 drift over 3*3912 steps)
     python tests/golden/make_golden_large.py rho0    # config A (nt = 393), heterogeneous rho0: rho0 and c0 gradients
-    python tests/golden/make_golden_large.py Dgrad   # config-D grid, 16 + 16 transducers next to Gamma, nt = 100 TR gradient
+    python tests/golden/make_golden_large.py Dgrad   # config-D grid, 16 + 16 transducers next to Gamma, nt = 28 TR gradient
     python tests/golden/make_golden_large.py E0      # config E level 0 (2 mm, 144x144x96), full nt = 978, observed = 0
 
 Every input is built exactly as bench.py / scenario.py build it (same seeds, same encoding

@@ -11,7 +11,7 @@ produced (oracle/_ref, tests/golden/make_golden_large.py; hours of fp64 CPU work
       after 3 * 3912 - 3 steps;
   config E level 0 (2 mm, 144 x 144 x 96) at its full nt = 978: traces and TR gradient;
   the TR gradient on the config-D grid (scenario.config_d_gradient_problem: the bench phantom,
-      16 + 16 transducers next to Gamma so that 100 steps already cross the 1.16 M-voxel shell).
+      16 + 16 transducers next to Gamma so that 28 steps already correlate inside Gamma).
 
 Bars (BASELINE.json north_star): traces rel l2 <= 1e-4, gradient rel l2 <= 1e-3."""
 import numpy as np
