@@ -19,6 +19,6 @@ ncu --set full --clock-control none --import-source on -k regex:"pencil_|zvel|zr
     -o gpurun_out/prof_full_$tag python scripts/prof_step.py --config D --nt 4 --grad > gpurun_out/ncu_full_$tag.log 2>&1
 echo "ncu full rc=$?"
 # the adjoint's correlating pressure kernel (pair loop only)
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:zp2_kernel<128, 16, 16, 1" -s 0 -c 1 \
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:zp2_kernel.*[(]bool[)]1, [(]bool[)]0" -s 0 -c 1 \
     -o gpurun_out/prof_corr_$tag python scripts/prof_step.py --config D --nt 4 --grad > gpurun_out/ncu_corr_$tag.log 2>&1
 echo "ncu corr rc=$?"
