@@ -1237,8 +1237,13 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR) zrho2_axis_kernel(const _
 #ifndef USTFWI_ZP_MINB
 #define USTFWI_ZP_MINB 8
 #endif
+// the correlating variant: 4 elements per load batch at 4 CTAs / SM (110 registers) measured
+// best on D200 (z-rho class 0.811 -> 0.803 ms; 2 at 6, 4 at 5 and 1 at 8 CTAs / SM measured)
 #ifndef USTFWI_ZPC_MINB
-#define USTFWI_ZPC_MINB 6
+#define USTFWI_ZPC_MINB 4
+#endif
+#ifndef USTFWI_ZPC_CHUNK
+#define USTFWI_ZPC_CHUNK 4
 #endif
 template <int M, int N1, int RW, bool CORR, bool STORE_P>
 __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR, CORR ? USTFWI_ZPC_MINB : USTFWI_ZP_MINB)
@@ -1312,7 +1317,8 @@ __global__ void __launch_bounds__(RW * Z2<M, N1>::TPR, CORR ? USTFWI_ZPC_MINB : 
         // knows, so without batching each element waits out its own load latency). Pairs at
         // the 64-register cap (8 CTAs / SM, USTFWI_ZP_MINB) measured best: D200 1.705 ->
         // 1.695 s / gradient; 4 / 8 per batch or an uncapped 80-96 registers were slower
-        constexpr int ZPC = N1 % USTFWI_ZP_CHUNK == 0 ? USTFWI_ZP_CHUNK : (N1 % 2 == 0 ? 2 : 1);
+        constexpr int CH = CORR ? USTFWI_ZPC_CHUNK : USTFWI_ZP_CHUNK;
+        constexpr int ZPC = N1 % CH == 0 ? CH : (N1 % 2 == 0 ? 2 : 1);
 #pragma unroll
         for (int j = 0; j < NA; ++j) {
             const int n2 = t + TPR * j;
